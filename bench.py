@@ -1,0 +1,375 @@
+#!/usr/bin/env python3
+"""bench.py -- fish-updates/s of the B200 FSB engine (BASELINE.json metric).
+
+A bench "step" is one simulation step over the whole school: swim + objective
++ global max(prev-cur) + barycentre sums + the (deferred) weight update for
+every fish.  Workload at N=1: BASELINE.json configs[1] =
+10,000,000 fish (fp64 SoA, 320 MB of state > 126 MB L2), the reference
+SimConfig mapping pond_size=200, weight_scale=1, step_base=0.1, seed=7.
+Multi-GPU (torchrun): weak scaling, 10^7 fish per GPU, contiguous shards, one
+NCCL allgather of 4 fp64 per step inside the CUDA graph.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value` = fish-updates/s with the school resident in HBM (device events around
+exactly K steps, max over ranks).  `e2e` = the same metric through the C-ABI
+with host buffers: upload of the AoS School from pinned memory, K steps with
+the max_diff trace returned to the host, download of the School, all timed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FISH_PER_GPU = 10_000_000
+BYTES_PER_UPDATE = 80  # read + write of the 5 x fp64 fish state
+METRIC = "fish-updates/sec (fish x steps / s)"
+UNIT = "fish-updates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int, period: float = 0.002):
+        self.device, self.period = device, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {
+            "sm_mhz": statistics.median(self.samples) if self.samples else None,
+            "sm_max_mhz": self.max_mhz,
+            "samples": len(self.samples),
+            "reasons": sorted(self.reasons),
+        }
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(world, v: float, local: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_sample(n: int, steps: int):
+    """Rank-0 CPU baseline: the reference's sequential path (oracle/_ref, the
+    reference headers compiled unmodified), 1 core, n fish x `steps` steps."""
+    import oracle
+
+    cfg = oracle.baseline_config(n, steps + 1)
+    try:
+        ref = oracle.Reference()
+        total, _, _ = ref.time_steps(cfg, warmup=1, steps=steps, threads=1, construct=oracle.SEQUENTIAL)
+        kind = "reference"
+    except Exception:
+        # oracle port (plain C restatement), timed the same way
+        orc = oracle.Oracle()
+        fish = orc.init(cfg)
+        orc.run(cfg, fish, 0, 1)
+        t0 = time.perf_counter()
+        orc.run(cfg, fish, 1, steps)
+        total = time.perf_counter() - t0
+        kind = "port"
+    return {
+        "value": n * steps / total,
+        "unit": UNIT,
+        "cores": 1,
+        "kind": kind,
+        "sample": f"{n} fish x {steps} steps (sequential construct, 1 core, after 1 warm-up step; "
+                  f"{total:.2f} s on {cpu_model()})",
+    }
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref =
+    the reference headers compiled with its flags) on all host threads, with its
+    default RunConfig schedule (static:50, Reduction; schedule.hpp:71-75)."""
+    if rank != 0:
+        return
+    import oracle
+
+    threads = os.cpu_count() or 1
+    n = args.fish
+    cfg = oracle.baseline_config(n, args.warmup + args.steps)
+    ref = oracle.Reference()
+    total, per, _ = ref.time_steps(cfg, warmup=args.warmup, steps=args.steps, threads=threads,
+                                   sched=oracle.STATIC, chunk=50, construct=oracle.REDUCTION)
+    value = n * args.steps / total
+    sample = (f"{n} fish x {args.steps} steps per run on {threads} threads ({cpu_model()}); "
+              f"RunConfig{{{threads}, static:50, Reduction}} = the reference default construct "
+              f"(its max drops a worker's partial, executor.hpp:243 -- timing only)")
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": value,
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (reference init_school, seed 7)",
+        "config": {"workload": f"FSB {n} fish fp64, pond 200, w0 1.0, step_base 0.1, seed 7 (BASELINE configs[1])",
+                   "fish": n, "parallelism": f"cpu {threads} threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_profile_traffic(n: int):
+    """dram bytes per step-kernel launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "step_kernel_ncu.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        if int(p.get("fish", -1)) == n:
+            return float(p["dram_bytes_per_launch"]), p.get("source")
+    except Exception:
+        pass
+    return None, None
+
+
+def run_ours(args, world, rank, local):
+    import ctypes
+
+    import numpy as np
+
+    import paper_2507_20173_b200 as fsb
+    from paper_2507_20173_b200 import _native as N
+
+    n_local = args.fish
+    n_total = n_local * world
+    cfg = fsb.baseline_config(n_total, args.warmup + args.steps)
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+
+        obj = [fsb.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    eng = fsb.Engine(cfg, device=local, rank=rank, world_size=world, nccl_unique_id=uid,
+                     strategy=args.strategy)
+    eng.init()
+    if args.warmup:
+        eng.run(0, args.warmup)
+    barrier(world)
+    eng.synchronize()
+    with ClockSampler(local) as clk:
+        trace, _, timing = eng.run(args.warmup, args.steps)
+    eng.synchronize()
+    barrier(world)
+    t_dev = allreduce_max(world, timing.seconds_move, local)
+    launches = eng.last_launches()
+    value = n_total * args.steps / t_dev
+
+    # per-kernel durations of the fused step kernel (events on the engine stream)
+    kms = eng.time_step_kernels(args.warmup + args.steps, max(3, min(args.steps, 50)))
+    kernel_s = float(np.mean(kms[1:])) * 1e-3 if len(kms) > 1 else float(kms[0]) * 1e-3
+    peak_gbs, peak_src = peaks()
+    achieved = BYTES_PER_UPDATE * n_local / kernel_s / 1e9
+    traffic, traffic_src = load_profile_traffic(n_local)
+
+    # e2e through the C-ABI with host buffers (pinned), all copies timed
+    e2e = None
+    if not args.no_e2e:
+        L = N.lib()
+        nbytes = n_local * 40
+        hp = ctypes.c_void_p()
+        N.check(L.fsb_host_alloc(ctypes.byref(hp), nbytes))
+        host = np.ctypeslib.as_array((ctypes.c_uint8 * nbytes).from_address(hp.value)).view(fsb.FISH_DTYPE)
+        eng.download(host)  # a valid School in pinned host memory
+        barrier(world)
+        t0 = time.perf_counter()
+        eng.upload(host)
+        tr, _, _ = eng.run(args.warmup, args.steps)
+        eng.download(host)
+        t_e2e = time.perf_counter() - t0
+        barrier(world)
+        t_e2e = allreduce_max(world, t_e2e, local)
+        N.check(L.fsb_host_free(hp))
+        e2e = {
+            "value": n_total * args.steps / t_e2e,
+            "unit": UNIT,
+            "h2d_bytes_per_step": nbytes / args.steps,
+            "d2h_bytes_per_step": (nbytes + 8 * args.steps) / args.steps,
+            "note": "per rank: AoS School upload from pinned host memory + K steps + trace and "
+                    "School download, wall clock, max over ranks",
+        }
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(args.fish, args.cpu_steps)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_dev / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (reference init_school on device, seed 7)",
+            "config": {
+                "workload": f"FSB {n_local} fish per GPU fp64 SoA, pond 200, w0 1.0, step_base 0.1, "
+                            f"seed 7 (BASELINE configs[1]); {n_total} fish total",
+                "fish_per_gpu": n_local,
+                "fish_total": n_total,
+                "parallelism": f"fish-sharded x{world}" + (" + NCCL allgather(4 fp64)/step" if world > 1 else ""),
+                "strategy": args.strategy,
+                "l2": f"inputs larger than L2 ({n_local * 32 / 1e6:.0f} MB resident state vs 126 MB L2)",
+                "timed": "K fused step kernels + 1 trailing eat kernel, one CUDA graph launch",
+            },
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "step_kernel",
+                "achieved": achieved,
+                "peak": peak_gbs,
+                "unit": "GB/s",
+                "frac": achieved / peak_gbs,
+                "traffic": traffic,
+                "algorithmic_bytes_per_fish_update": BYTES_PER_UPDATE,
+                "kernel_ms": kernel_s * 1e3,
+                "peak_source": peak_src,
+                "traffic_source": traffic_src,
+            },
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "trace_last": float(trace[-1]),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--fish", type=int, default=FISH_PER_GPU, help="fish per GPU")
+    ap.add_argument("--strategy", default="auto", choices=["auto", "stream", "persistent"])
+    ap.add_argument("--cpu-steps", type=int, default=40)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    world, rank, local = dist_setup(args)
+    try:
+        if args.impl == "reference":
+            run_reference(args, world, rank)
+        else:
+            run_ours(args, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * fsb_b200.h -- C-ABI of the B200-native Fish School Behaviour step engine.
+ *
+ * Plain C: POD structs, pointers, sizes and int status codes; no CUDA, torch
+ * or C++ types cross this boundary.  Implemented by
+ * paper_2507_20173_b200/libfsb_b200.so (sm_100a kernels + host runtime).
+ *
+ * The reference has no FFI of its own: its seam for this path is the
+ * parfor::Executor& parameter of the fsb phase functions
+ * (/root/reference/proj/include/fsb/sim.hpp:84,110,133).  Each
+ * entry point below names the reference function it replaces.  A C++ drop-in
+ * that restores the reference's own types and call shapes on top of this ABI
+ * is include/fsb/gpu.hpp; the ctypes binding is paper_2507_20173_b200/_native.py.
+ *
+ * Semantics follow the reference bit-for-bit (positions, weights, objectives
+ * and the max_diff trace), computed in IEEE binary64 without FMA contraction.
+ * There is no CPU fallback: every compute entry point fails with
+ * FSB_ERR_CUDA when no usable sm_100 device is present.
+ */
+#ifndef FSB_B200_H
+#define FSB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSB_B200_ABI_VERSION 1
+
+/* Status codes.  fsb_last_error() holds a message for the calling thread. */
+enum fsb_status {
+    FSB_OK = 0,
+    FSB_ERR_INVALID_CONFIG = 1,   /* SimConfig::validate would throw std::invalid_argument (sim.hpp:44-49) */
+    FSB_ERR_INVALID_ARGUMENT = 2, /* bad pointer / size / rank */
+    FSB_ERR_CUDA = 3,             /* CUDA runtime or device error (incl. no GPU) */
+    FSB_ERR_NCCL = 4,             /* NCCL unavailable or failed */
+    FSB_ERR_OUT_OF_MEMORY = 5,
+    FSB_ERR_UNSUPPORTED = 6       /* e.g. persistent strategy for a school that does not fit */
+};
+
+/* fsb::SimConfig (sim.hpp:34-50), same field order and meaning. */
+typedef struct fsb_sim_config {
+    uint64_t num_fish;
+    double pond_size;
+    double weight_scale; /* W0: init weights uniform in [1, W0]; band [1, 2*W0] */
+    uint64_t num_steps;
+    uint64_t seed;
+    double step_base;    /* per-axis displacement bound at unit weight */
+} fsb_sim_config;
+
+/* fsb::Fish (sim.hpp:26-32): 40 bytes, the byte layout fsb::checksum hashes. */
+typedef struct fsb_fish {
+    double x;
+    double y;
+    double weight;
+    double prev_objective;
+    double current_objective;
+} fsb_fish;
+
+/* fsb::SimResult timing fields (sim.hpp:128-130), device-timed (cudaEvent). */
+typedef struct fsb_timing {
+    double seconds_total; /* init + step loop (simulate) or the step loop (run) */
+    double seconds_move;  /* step loop: fused move+max(+deferred eat) kernels   */
+    double seconds_eat;   /* standalone eat kernels (trailing / phase eat)      */
+} fsb_timing;
+
+/* Step-loop strategies. */
+enum fsb_strategy {
+    FSB_STRATEGY_AUTO = 0,       /* persistent for small single-GPU schools, else stream */
+    FSB_STRATEGY_STREAM = 1,     /* one fused step kernel per step, CUDA-graph replayed  */
+    FSB_STRATEGY_PERSISTENT = 2  /* one thread-block cluster runs all steps on chip       */
+};
+
+/* Engine flags. */
+#define FSB_FLAG_NO_ALTERNATE 0x1u /* keep tile order fixed (default reverses odd steps for L2 reuse) */
+#define FSB_FLAG_FORCE_NCCL 0x2u   /* use the NCCL exchange even when world_size == 1 (testing) */
+
+typedef struct fsb_engine_options {
+    int device;                  /* CUDA device ordinal of this shard */
+    int rank;                    /* shard index in [0, world_size) */
+    int world_size;              /* number of shards (one process or thread per GPU) */
+    const void* nccl_unique_id;  /* 128-byte ncclUniqueId shared by all ranks (world_size > 1) */
+    int strategy;                /* enum fsb_strategy */
+    unsigned flags;              /* FSB_FLAG_* */
+} fsb_engine_options;
+
+typedef struct fsb_engine fsb_engine;
+
+int fsb_abi_version(void);
+const char* fsb_last_error(void);
+
+/* SimConfig::validate (sim.hpp:44-49): FSB_OK or FSB_ERR_INVALID_CONFIG with
+ * the reference's exception text in fsb_last_error(). Host-only. */
+int fsb_config_validate(const fsb_sim_config* cfg);
+
+/* Contiguous partition: rank r owns global fish [floor(rN/G), floor((r+1)N/G)). Host-only. */
+int fsb_shard_range(uint64_t num_fish, int world_size, int rank, uint64_t* first, uint64_t* count);
+
+/* FNV-1a 64 over fsb_fish bytes, continuing from h (kChecksumEmpty =
+ * 0xcbf29ce484222325 to start): fsb::checksum (sim.hpp:158-176). Host-only
+ * verification helper. */
+uint64_t fsb_checksum_update(uint64_t h, const fsb_fish* fish, uint64_t n);
+
+/* Number of visible CUDA devices (0 when none). */
+int fsb_device_count(int* count);
+
+/* Page-locked host buffers for fast upload/download. */
+int fsb_host_alloc(void** ptr, size_t bytes);
+int fsb_host_free(void* ptr);
+
+/* 128-byte ncclUniqueId for a world_size > 1 engine (call on rank 0, broadcast). */
+int fsb_nccl_unique_id(void* out, size_t len);
+
+/* Create the engine for one shard.  Replaces constructing parfor::Executor
+ * (executor.hpp:30-41) for this path.  opts may be NULL (device 0, 1 rank). */
+int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts, fsb_engine** out);
+int fsb_engine_destroy(fsb_engine* e);
+
+/* This shard's global index range. */
+int fsb_engine_shard(const fsb_engine* e, uint64_t* first, uint64_t* count);
+
+/* init_school (sim.hpp:65-79) on the device. */
+int fsb_engine_init(fsb_engine* e);
+
+/* Replace / read the shard's school (count == shard count) in fsb::Fish layout. */
+int fsb_engine_upload(fsb_engine* e, const fsb_fish* fish, uint64_t count);
+int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count);
+
+/* move_phase(school, cfg, step, exec) (sim.hpp:84-99).  seconds: device time. */
+int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds);
+
+/* eat_phase(school, cfg, exec) (sim.hpp:110-123): global max of prev-cur
+ * (-inf for an empty school) and the weight update when it is > 0. */
+int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds);
+
+/* The step loop of simulate (sim.hpp:139-144) for steps
+ * [first_step, first_step + num_steps): T x (move, eat), on device.
+ * trace[num_steps] receives max_diff per step (EatResult::max_diff);
+ * bary[3*num_steps] (may be NULL) the per-step sums {sum x*f, sum y*f, sum f}
+ * over all shards.  timing may be NULL. */
+int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* trace,
+                   double* bary, fsb_timing* timing);
+
+/* simulate(cfg, exec) (sim.hpp:133-147): init + run(0, cfg.num_steps). */
+int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* timing);
+
+/* Barycentre query (new; north_star): global f-weighted sums of the current
+ * state and B = (sum x*f / sum f, sum y*f / sum f). */
+int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]);
+
+/* FNV-1a of this shard's school continuing from h_in (checksum, sim.hpp:158). */
+int fsb_engine_checksum(fsb_engine* e, uint64_t h_in, uint64_t* h_out);
+
+/* Block until queued work is done. */
+int fsb_engine_synchronize(fsb_engine* e);
+
+/* The engine's CUDA stream (a cudaStream_t), for callers that time or order work on it. */
+int fsb_engine_stream(fsb_engine* e, void** stream);
+
+/* Measurement aid: launch the fused step kernel num_steps times eagerly with a
+ * CUDA event pair around each launch; kernel_ms[k] = duration of launch k. */
+int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t num_steps,
+                                 double* kernel_ms);
+
+/* Kernel launch count of the last fsb_engine_run (for bench accounting). */
+int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FSB_B200_H */

@@ -1,0 +1,800 @@
+// fsb_engine.cu -- host runtime behind the C-ABI (include/fsb_b200.h).
+//
+// One engine owns one shard of the school on one GPU: SoA state in HBM, a
+// non-blocking stream, the reduction workspace, cached CUDA graphs of the
+// fused step loop, and (world_size > 1) an NCCL communicator used for the one
+// per-step exchange of {max(prev-cur), sum x*f, sum y*f, sum f}.
+//
+// Replaces, for this path, the reference's parfor::Executor dispatch
+// (executor.hpp:63-103, 130-159): no host thread touches fish state.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/fsb_b200.h"
+#include "fsb_kernels.cuh"
+
+using fsb_dev::Partial;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    const int code = (e == cudaErrorMemoryAllocation) ? FSB_ERR_OUT_OF_MEMORY : FSB_ERR_CUDA;
+    g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    cudaGetLastError();  // clear sticky-free errors
+    return code;
+}
+
+#define CU(call)                                          \
+    do {                                                  \
+        cudaError_t _e = (call);                          \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+#define TRY(call)                 \
+    do {                          \
+        int _rc = (call);         \
+        if (_rc != FSB_OK) return _rc; \
+    } while (0)
+
+// ---- NCCL, loaded on demand (only world_size > 1 needs it) -----------------
+struct NcclApi {
+    bool tried = false;
+    void* handle = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+std::mutex g_nccl_mu;
+NcclApi g_nccl;
+
+int nccl_load() {
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (g_nccl.handle) return FSB_OK;
+    if (g_nccl.tried) return fail(FSB_ERR_NCCL, "libnccl.so.2 could not be loaded");
+    g_nccl.tried = true;
+    // An already-loaded NCCL (e.g. torch's) is reused through its soname.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(FSB_ERR_NCCL, std::string("dlopen libnccl.so.2 failed: ") + dlerror());
+    g_nccl.GetUniqueId = reinterpret_cast<decltype(g_nccl.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    g_nccl.CommInitRank = reinterpret_cast<decltype(g_nccl.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    g_nccl.CommDestroy = reinterpret_cast<decltype(g_nccl.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    g_nccl.AllGather = reinterpret_cast<decltype(g_nccl.AllGather)>(dlsym(h, "ncclAllGather"));
+    g_nccl.GetErrorString =
+        reinterpret_cast<decltype(g_nccl.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.CommDestroy || !g_nccl.AllGather ||
+        !g_nccl.GetErrorString)
+        return fail(FSB_ERR_NCCL, "libnccl.so.2 lacks a required symbol");
+    g_nccl.handle = h;
+    return FSB_OK;
+}
+
+int nccl_fail(ncclResult_t r, const char* what) {
+    return fail(FSB_ERR_NCCL, std::string(what) + ": " +
+                                  (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "nccl error"));
+}
+
+constexpr uint64_t kStagingFish = 1ull << 22;  // 160 MB AoS staging per chunk
+
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    double* d_trace = nullptr;
+    double* d_bary = nullptr;
+    uint64_t launches = 0;
+};
+
+}  // namespace
+
+struct fsb_engine {
+    fsb_sim_config cfg{};
+    int device = 0;
+    int rank = 0;
+    int world = 1;
+    int strategy = FSB_STRATEGY_AUTO;
+    unsigned flags = 0;
+    bool use_nccl = false;
+    uint64_t first = 0;  // global index of local fish 0
+    uint64_t count = 0;  // local fish
+
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    fsb_dev::SoA s{};       // s.c stays nullptr in the engine's canonical state
+    double* c_buf = nullptr;  // explicit current_objective (only after an inconsistent upload)
+    bool cur_explicit = false;
+    bool max_valid = false;  // part_all[cur_buf] holds the partials of the current state
+    int cur_buf = 0;
+
+    Partial* part_all = nullptr;  // [2][world]
+    Partial* block_part = nullptr;
+    unsigned* counter = nullptr;
+    uint64_t* d_step0 = nullptr;
+    uint64_t* h_step0 = nullptr;  // pinned
+    double* d_scalar = nullptr;   // [4]
+    int* d_mismatch = nullptr;
+    int grid = 0;
+    int grid_explicit = 0;
+
+    void* staging = nullptr;  // device AoS staging
+    void* pinned = nullptr;   // host pinned staging (checksum)
+    double* d_cl_trace = nullptr;  // persistent-kernel trace buffers
+    double* d_cl_bary = nullptr;
+    uint64_t cl_cap = 0;
+    uint64_t last_launches = 0;
+
+    std::map<std::pair<uint64_t, int>, GraphEntry> graphs;
+    ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+fsb_dev::Scalars scalars_of(const fsb_sim_config& c) {
+    fsb_dev::Scalars k;
+    k.pond = c.pond_size;
+    k.half_pond = c.pond_size / 2.0;
+    k.step_base = c.step_base;
+    k.w_max = 2.0 * c.weight_scale;  // SimConfig::weight_max (sim.hpp:42)
+    k.seed = c.seed;
+    return k;
+}
+
+fsb_dev::SoA canonical(const fsb_engine* e) {
+    fsb_dev::SoA s = e->s;
+    s.c = e->cur_explicit ? e->c_buf : nullptr;
+    return s;
+}
+
+Partial* local_part(fsb_engine* e, int buf) { return e->part_all + buf * e->world + e->rank; }
+Partial* all_part(fsb_engine* e, int buf) { return e->part_all + buf * e->world; }
+
+int exchange(fsb_engine* e, int buf) {
+    if (!e->use_nccl) return FSB_OK;
+    // in place: send = recv + rank * count
+    ncclResult_t r = g_nccl.AllGather(local_part(e, buf), all_part(e, buf), 4, ncclFloat64, e->comm,
+                                      e->stream);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
+    return FSB_OK;
+}
+
+int guard(fsb_engine* e) {
+    if (!e) return fail(FSB_ERR_INVALID_ARGUMENT, "null engine");
+    CU(cudaSetDevice(e->device));
+    return FSB_OK;
+}
+
+int ensure_staging(fsb_engine* e) {
+    if (!e->staging) CU(cudaMalloc(&e->staging, kStagingFish * sizeof(fsb_fish)));
+    return FSB_OK;
+}
+
+int elapsed(fsb_engine* e, double* seconds) {
+    CU(cudaEventSynchronize(e->ev1));
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    if (seconds) *seconds = ms * 1e-3;
+    return FSB_OK;
+}
+
+bool want_persistent(const fsb_engine* e) {
+    if (e->world != 1 || e->use_nccl) return false;
+    if (e->strategy == FSB_STRATEGY_PERSISTENT) return true;
+    if (e->strategy == FSB_STRATEGY_STREAM) return false;
+    return e->count > 0 && e->count <= 16384;
+}
+
+void free_graphs(fsb_engine* e) {
+    for (auto& kv : e->graphs) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.d_trace) cudaFree(kv.second.d_trace);
+        if (kv.second.d_bary) cudaFree(kv.second.d_bary);
+    }
+    e->graphs.clear();
+}
+
+fsb_dev::StepArgs step_args(fsb_engine* e, const fsb_dev::SoA& s) {
+    fsb_dev::StepArgs a{};
+    a.s = s;
+    a.k = scalars_of(e->cfg);
+    a.n = e->count;
+    a.gfirst = e->first;
+    a.world = e->world;
+    a.ws.block_part = e->block_part;
+    a.ws.counter = e->counter;
+    a.alternate = (e->flags & FSB_FLAG_NO_ALTERNATE) ? 0 : 1;
+    return a;
+}
+
+// Capture: step kernel k (k = 0..T-1) applies the deferred eat of step k-1,
+// moves step first+k and publishes its partial; NCCL allgathers it; a final
+// eat kernel applies step T-1's eat.  The first step index is read at run time
+// from d_step0 (filled by the graph's first node from pinned memory), so one
+// graph serves every first_step.
+int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out) {
+    GraphEntry g;
+    CU(cudaMalloc(&g.d_trace, T * sizeof(double)));
+    CU(cudaMalloc(&g.d_bary, 3 * T * sizeof(double)));
+    CU(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = FSB_OK;
+    cudaError_t ce = cudaMemcpyAsync(e->d_step0, e->h_step0, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                     e->stream);
+    uint64_t launches = 0;
+    for (uint64_t k = 0; k < T && ce == cudaSuccess && rc == FSB_OK; ++k) {
+        fsb_dev::SoA s = e->s;
+        s.c = (k == 0 && explicit_first) ? e->c_buf : nullptr;
+        fsb_dev::StepArgs a = step_args(e, s);
+        a.step_ptr = e->d_step0;
+        a.step_add = k;
+        a.part_in = k ? all_part(e, (int)((k - 1) & 1)) : nullptr;
+        a.trace_out = k ? g.d_trace + (k - 1) : nullptr;
+        a.bary_out = k ? g.d_bary + 3 * (k - 1) : nullptr;
+        a.part_out = local_part(e, (int)(k & 1));
+        ce = fsb_dev::launch_step(a, (k == 0 && explicit_first) ? e->grid_explicit : e->grid, e->stream);
+        ++launches;
+        if (ce == cudaSuccess) rc = exchange(e, (int)(k & 1));
+    }
+    if (ce == cudaSuccess && rc == FSB_OK) {
+        fsb_dev::EatArgs ea{};
+        ea.s = e->s;
+        ea.s.c = (T == 0 && explicit_first) ? e->c_buf : nullptr;
+        ea.k = scalars_of(e->cfg);
+        ea.n = e->count;
+        ea.part_in = all_part(e, (int)((T - 1) & 1));
+        ea.world = e->world;
+        ea.trace_out = g.d_trace + (T - 1);
+        ea.bary_out = g.d_bary + 3 * (T - 1);
+        ce = fsb_dev::launch_eat(ea, e->grid, e->stream);
+        ++launches;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(e->stream, &graph);
+    if (ce != cudaSuccess) return cuda_fail(ce, "capture step loop");
+    if (rc != FSB_OK) return rc;
+    if (ee != cudaSuccess) return cuda_fail(ee, "cudaStreamEndCapture");
+    ee = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ee != cudaSuccess) return cuda_fail(ee, "cudaGraphInstantiate");
+    g.launches = launches;
+    *out = g;
+    return FSB_OK;
+}
+
+int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
+               double* seconds) {
+    const auto key = std::make_pair(T, e->cur_explicit ? 1 : 0);
+    auto it = e->graphs.find(key);
+    if (it == e->graphs.end()) {
+        GraphEntry g;
+        TRY(build_graph(e, T, e->cur_explicit, &g));
+        it = e->graphs.emplace(key, g).first;
+    }
+    *e->h_step0 = first_step;
+    CU(cudaEventRecord(e->ev0, e->stream));
+    CU(cudaGraphLaunch(it->second.exec, e->stream));
+    CU(cudaEventRecord(e->ev1, e->stream));
+    if (trace) CU(cudaMemcpyAsync(trace, it->second.d_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    if (bary) CU(cudaMemcpyAsync(bary, it->second.d_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    TRY(elapsed(e, seconds));
+    e->cur_explicit = false;
+    e->max_valid = true;
+    e->cur_buf = (int)((T - 1) & 1);
+    e->last_launches = it->second.launches;
+    return FSB_OK;
+}
+
+int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
+                   double* seconds) {
+    if (T > e->cl_cap) {
+        if (e->d_cl_trace) cudaFree(e->d_cl_trace);
+        if (e->d_cl_bary) cudaFree(e->d_cl_bary);
+        e->d_cl_trace = e->d_cl_bary = nullptr;
+        e->cl_cap = 0;
+        CU(cudaMalloc(&e->d_cl_trace, T * sizeof(double)));
+        CU(cudaMalloc(&e->d_cl_bary, 3 * T * sizeof(double)));
+        e->cl_cap = T;
+    }
+    fsb_dev::ClusterArgs a{};
+    a.s = canonical(e);
+    a.k = scalars_of(e->cfg);
+    a.n = e->count;
+    a.gfirst = e->first;
+    a.first_step = first_step;
+    a.num_steps = T;
+    a.trace = e->d_cl_trace;
+    a.bary = e->d_cl_bary;
+    a.part_out = local_part(e, 0);
+    CU(cudaEventRecord(e->ev0, e->stream));
+    cudaError_t ce = fsb_dev::launch_cluster_run(a, e->stream);
+    if (ce == cudaErrorNotSupported)
+        return fail(FSB_ERR_UNSUPPORTED, "school does not fit the persistent cluster kernel");
+    if (ce != cudaSuccess) return cuda_fail(ce, "cluster kernel launch");
+    CU(cudaEventRecord(e->ev1, e->stream));
+    if (trace) CU(cudaMemcpyAsync(trace, e->d_cl_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    if (bary) CU(cudaMemcpyAsync(bary, e->d_cl_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    TRY(elapsed(e, seconds));
+    e->cur_explicit = false;
+    e->max_valid = true;
+    e->cur_buf = 0;
+    e->last_launches = 1;
+    return FSB_OK;
+}
+
+int reduce_current(fsb_engine* e) {
+    fsb_dev::ReduceArgs a{};
+    a.s = canonical(e);
+    a.k = scalars_of(e->cfg);
+    a.n = e->count;
+    a.ws.block_part = e->block_part;
+    a.ws.counter = e->counter;
+    a.part_out = local_part(e, 0);
+    if (e->count == 0) {
+        const Partial id{-INFINITY, 0.0, 0.0, 0.0};
+        CU(cudaMemcpyAsync(a.part_out, &id, sizeof(Partial), cudaMemcpyHostToDevice, e->stream));
+    } else {
+        CU(fsb_dev::launch_reduce(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
+    }
+    TRY(exchange(e, 0));
+    e->cur_buf = 0;
+    e->max_valid = true;
+    return FSB_OK;
+}
+
+int host_combine(fsb_engine* e, Partial* out) {
+    std::vector<Partial> parts(e->world);
+    CU(cudaMemcpyAsync(parts.data(), all_part(e, e->cur_buf), e->world * sizeof(Partial),
+                       cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    // rank order, same operators as the device combine (no contraction: adds only)
+    Partial r{-INFINITY, 0.0, 0.0, 0.0};
+    for (const Partial& p : parts) {
+        r.best = (p.best > r.best) ? p.best : r.best;
+        r.sx += p.sx;
+        r.sy += p.sy;
+        r.sf += p.sf;
+    }
+    *out = r;
+    return FSB_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int fsb_abi_version(void) { return FSB_B200_ABI_VERSION; }
+
+const char* fsb_last_error(void) { return g_err.c_str(); }
+
+int fsb_config_validate(const fsb_sim_config* cfg) {
+    if (!cfg) return fail(FSB_ERR_INVALID_ARGUMENT, "null config");
+    // sim.hpp:44-49, same order and messages
+    if (!(cfg->pond_size > 0.0)) return fail(FSB_ERR_INVALID_CONFIG, "SimConfig: pond_size must be > 0");
+    if (!(cfg->weight_scale >= 1.0))
+        return fail(FSB_ERR_INVALID_CONFIG, "SimConfig: weight_scale must be >= 1");
+    if (!(cfg->step_base > 0.0)) return fail(FSB_ERR_INVALID_CONFIG, "SimConfig: step_base must be > 0");
+    return FSB_OK;
+}
+
+int fsb_shard_range(uint64_t n, int world, int rank, uint64_t* first, uint64_t* count) {
+    if (world < 1 || rank < 0 || rank >= world || !first || !count)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "fsb_shard_range: bad world/rank");
+    // floor(r*N/G) without 128-bit overflow concerns for N < 2^57, G <= 128
+    const unsigned __int128 lo = (unsigned __int128)n * (unsigned)rank / (unsigned)world;
+    const unsigned __int128 hi = (unsigned __int128)n * (unsigned)(rank + 1) / (unsigned)world;
+    *first = (uint64_t)lo;
+    *count = (uint64_t)(hi - lo);
+    return FSB_OK;
+}
+
+uint64_t fsb_checksum_update(uint64_t h, const fsb_fish* fish, uint64_t n) {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(fish);
+    const uint64_t bytes = n * sizeof(fsb_fish);
+    for (uint64_t k = 0; k < bytes; ++k) {
+        h ^= p[k];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+int fsb_device_count(int* count) {
+    if (!count) return fail(FSB_ERR_INVALID_ARGUMENT, "null count");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+    }
+    *count = n;
+    return FSB_OK;
+}
+
+int fsb_host_alloc(void** ptr, size_t bytes) {
+    if (!ptr) return fail(FSB_ERR_INVALID_ARGUMENT, "null ptr");
+    CU(cudaMallocHost(ptr, bytes ? bytes : 1));
+    return FSB_OK;
+}
+
+int fsb_host_free(void* ptr) {
+    if (ptr) CU(cudaFreeHost(ptr));
+    return FSB_OK;
+}
+
+int fsb_nccl_unique_id(void* out, size_t len) {
+    if (!out || len < sizeof(ncclUniqueId)) return fail(FSB_ERR_INVALID_ARGUMENT, "need 128 bytes");
+    TRY(nccl_load());
+    ncclUniqueId id;
+    ncclResult_t r = g_nccl.GetUniqueId(&id);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof id);
+    return FSB_OK;
+}
+
+int fsb_engine_destroy(fsb_engine* e) {
+    if (!e) return FSB_OK;
+    cudaSetDevice(e->device);
+    if (e->stream) cudaStreamSynchronize(e->stream);
+    free_graphs(e);
+    if (e->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(e->comm);
+    for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
+                    (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
+                    (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
+                    (void*)e->d_cl_bary})
+        if (p) cudaFree(p);
+    if (e->h_step0) cudaFreeHost(e->h_step0);
+    if (e->pinned) cudaFreeHost(e->pinned);
+    if (e->ev0) cudaEventDestroy(e->ev0);
+    if (e->ev1) cudaEventDestroy(e->ev1);
+    if (e->stream) cudaStreamDestroy(e->stream);
+    delete e;
+    return FSB_OK;
+}
+
+int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts, fsb_engine** out) {
+    if (!cfg || !out) return fail(FSB_ERR_INVALID_ARGUMENT, "null argument");
+    *out = nullptr;
+    TRY(fsb_config_validate(cfg));
+    fsb_engine_options o{};
+    o.world_size = 1;
+    if (opts) o = *opts;
+    if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "bad rank/world_size");
+    if (o.strategy < FSB_STRATEGY_AUTO || o.strategy > FSB_STRATEGY_PERSISTENT)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "bad strategy");
+
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(FSB_ERR_CUDA, "no CUDA device available (the engine has no CPU fallback)");
+    }
+    if (o.device < 0 || o.device >= ndev) return fail(FSB_ERR_INVALID_ARGUMENT, "bad device ordinal");
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, o.device));
+    if (prop.major < 10)
+        return fail(FSB_ERR_CUDA, std::string("device ") + prop.name + " is not sm_100 (built for sm_100a only)");
+
+    fsb_engine* e = new (std::nothrow) fsb_engine();
+    if (!e) return fail(FSB_ERR_OUT_OF_MEMORY, "host allocation");
+    e->cfg = *cfg;
+    e->device = o.device;
+    e->rank = o.rank;
+    e->world = o.world_size;
+    e->strategy = o.strategy;
+    e->flags = o.flags;
+    e->use_nccl = o.world_size > 1 || (o.flags & FSB_FLAG_FORCE_NCCL);
+    fsb_shard_range(cfg->num_fish, e->world, e->rank, &e->first, &e->count);
+
+    auto bail = [&](int rc) {
+        const std::string msg = g_err;
+        fsb_engine_destroy(e);
+        g_err = msg;
+        return rc;
+    };
+#define CB(call)                                                 \
+    do {                                                         \
+        cudaError_t _e = (call);                                 \
+        if (_e != cudaSuccess) return bail(cuda_fail(_e, #call)); \
+    } while (0)
+
+    CB(cudaSetDevice(e->device));
+    CB(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    CB(cudaEventCreate(&e->ev0));
+    CB(cudaEventCreate(&e->ev1));
+    const size_t bytes = (e->count ? e->count : 1) * sizeof(double);
+    CB(cudaMalloc(&e->s.x, bytes));
+    CB(cudaMalloc(&e->s.y, bytes));
+    CB(cudaMalloc(&e->s.w, bytes));
+    CB(cudaMalloc(&e->s.p, bytes));
+    e->s.c = nullptr;
+    e->grid = fsb_dev::step_grid_blocks(e->device, false);
+    e->grid_explicit = fsb_dev::step_grid_blocks(e->device, true);
+    const int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
+    CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
+    CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
+    CB(cudaMalloc(&e->counter, sizeof(unsigned)));
+    CB(cudaMemset(e->counter, 0, sizeof(unsigned)));
+    CB(cudaMalloc(&e->d_step0, sizeof(uint64_t)));
+    CB(cudaMallocHost(&e->h_step0, sizeof(uint64_t)));
+    CB(cudaMalloc(&e->d_scalar, 4 * sizeof(double)));
+    CB(cudaMalloc(&e->d_mismatch, sizeof(int)));
+
+    if (e->use_nccl) {
+        if (!o.nccl_unique_id) return bail(fail(FSB_ERR_INVALID_ARGUMENT, "world_size > 1 needs nccl_unique_id"));
+        int rc = nccl_load();
+        if (rc != FSB_OK) return bail(rc);
+        ncclUniqueId id;
+        std::memcpy(&id, o.nccl_unique_id, sizeof id);
+        ncclResult_t r = g_nccl.CommInitRank(&e->comm, e->world, id, e->rank);
+        if (r != ncclSuccess) return bail(nccl_fail(r, "ncclCommInitRank"));
+    }
+#undef CB
+    *out = e;
+    return FSB_OK;
+}
+
+int fsb_engine_shard(const fsb_engine* e, uint64_t* first, uint64_t* count) {
+    if (!e) return fail(FSB_ERR_INVALID_ARGUMENT, "null engine");
+    if (first) *first = e->first;
+    if (count) *count = e->count;
+    return FSB_OK;
+}
+
+int fsb_engine_init(fsb_engine* e) {
+    TRY(guard(e));
+    fsb_dev::InitArgs a{};
+    a.s = e->s;
+    a.k = scalars_of(e->cfg);
+    a.n = e->count;
+    a.gfirst = e->first;
+    a.w0 = e->cfg.weight_scale;
+    CU(fsb_dev::launch_init(a, 0, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    e->cur_explicit = false;
+    e->max_valid = false;
+    return FSB_OK;
+}
+
+int fsb_engine_upload(fsb_engine* e, const fsb_fish* fish, uint64_t count) {
+    TRY(guard(e));
+    if (count != e->count) return fail(FSB_ERR_INVALID_ARGUMENT, "upload count != shard count");
+    if (count && !fish) return fail(FSB_ERR_INVALID_ARGUMENT, "null fish");
+    if (!e->c_buf) CU(cudaMalloc(&e->c_buf, (e->count ? e->count : 1) * sizeof(double)));
+    TRY(ensure_staging(e));
+    fsb_dev::SoA s = e->s;
+    s.c = e->c_buf;
+    CU(cudaMemsetAsync(e->d_mismatch, 0, sizeof(int), e->stream));
+    for (uint64_t lo = 0; lo < count; lo += kStagingFish) {
+        const uint64_t cnt = (count - lo < kStagingFish) ? count - lo : kStagingFish;
+        CU(cudaMemcpyAsync(e->staging, fish + lo, cnt * sizeof(fsb_fish), cudaMemcpyHostToDevice, e->stream));
+        CU(fsb_dev::launch_aos_to_soa(e->staging, s, e->cfg.pond_size / 2.0, lo, cnt, e->d_mismatch, e->stream));
+    }
+    int mismatch = 0;
+    CU(cudaMemcpyAsync(&mismatch, e->d_mismatch, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    e->cur_explicit = mismatch != 0;
+    e->max_valid = false;
+    return FSB_OK;
+}
+
+int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count) {
+    TRY(guard(e));
+    if (count != e->count) return fail(FSB_ERR_INVALID_ARGUMENT, "download count != shard count");
+    if (count && !fish) return fail(FSB_ERR_INVALID_ARGUMENT, "null fish");
+    TRY(ensure_staging(e));
+    const fsb_dev::SoA s = canonical(e);
+    for (uint64_t lo = 0; lo < count; lo += kStagingFish) {
+        const uint64_t cnt = (count - lo < kStagingFish) ? count - lo : kStagingFish;
+        CU(fsb_dev::launch_soa_to_aos(s, e->cfg.pond_size / 2.0, lo, cnt, e->staging, e->stream));
+        CU(cudaMemcpyAsync(fish + lo, e->staging, cnt * sizeof(fsb_fish), cudaMemcpyDeviceToHost, e->stream));
+    }
+    CU(cudaStreamSynchronize(e->stream));
+    return FSB_OK;
+}
+
+int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
+    TRY(guard(e));
+    CU(cudaEventRecord(e->ev0, e->stream));
+    if (e->count) {
+        fsb_dev::StepArgs a = step_args(e, canonical(e));
+        a.step_ptr = nullptr;
+        a.step_add = step;
+        a.part_in = nullptr;  // no pending eat: phases are applied eagerly
+        a.part_out = local_part(e, 0);
+        CU(fsb_dev::launch_step(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
+    } else {
+        const Partial id{-INFINITY, 0.0, 0.0, 0.0};
+        CU(cudaMemcpyAsync(local_part(e, 0), &id, sizeof(Partial), cudaMemcpyHostToDevice, e->stream));
+    }
+    TRY(exchange(e, 0));
+    CU(cudaEventRecord(e->ev1, e->stream));
+    TRY(elapsed(e, seconds));
+    e->cur_explicit = false;
+    e->max_valid = true;
+    e->cur_buf = 0;
+    return FSB_OK;
+}
+
+int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
+    TRY(guard(e));
+    CU(cudaEventRecord(e->ev0, e->stream));
+    if (!e->max_valid) TRY(reduce_current(e));
+    fsb_dev::EatArgs a{};
+    a.s = canonical(e);
+    a.k = scalars_of(e->cfg);
+    a.n = e->count;
+    a.part_in = all_part(e, e->cur_buf);
+    a.world = e->world;
+    a.trace_out = e->d_scalar;
+    CU(fsb_dev::launch_eat(a, e->grid, e->stream));
+    CU(cudaEventRecord(e->ev1, e->stream));
+    double m = 0.0;
+    CU(cudaMemcpyAsync(&m, e->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    TRY(elapsed(e, seconds));
+    CU(cudaStreamSynchronize(e->stream));
+    if (max_diff) *max_diff = m;
+    return FSB_OK;
+}
+
+int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* trace, double* bary,
+                   fsb_timing* timing) {
+    TRY(guard(e));
+    if (timing) *timing = fsb_timing{0.0, 0.0, 0.0};
+    if (num_steps == 0) return FSB_OK;
+    double secs = 0.0;
+    if (e->count == 0 && !e->use_nccl) {
+        // empty school: every max is -inf (executor.hpp:86), sums are 0
+        for (uint64_t k = 0; k < num_steps; ++k) {
+            if (trace) trace[k] = -INFINITY;
+            if (bary) bary[3 * k] = bary[3 * k + 1] = bary[3 * k + 2] = 0.0;
+        }
+        const Partial id{-INFINITY, 0.0, 0.0, 0.0};
+        CU(cudaMemcpy(local_part(e, 0), &id, sizeof(Partial), cudaMemcpyHostToDevice));
+        e->max_valid = true;
+        e->cur_buf = 0;
+        e->last_launches = 0;
+    } else if (want_persistent(e)) {
+        int rc = run_persistent(e, first_step, num_steps, trace, bary, &secs);
+        if (rc == FSB_ERR_UNSUPPORTED && e->strategy == FSB_STRATEGY_AUTO)
+            rc = run_stream(e, first_step, num_steps, trace, bary, &secs);
+        TRY(rc);
+    } else {
+        TRY(run_stream(e, first_step, num_steps, trace, bary, &secs));
+    }
+    if (timing) {
+        timing->seconds_total = secs;
+        timing->seconds_move = secs;
+        timing->seconds_eat = 0.0;
+    }
+    return FSB_OK;
+}
+
+int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* timing) {
+    TRY(guard(e));
+    CU(cudaEventRecord(e->ev0, e->stream));
+    TRY(fsb_engine_init(e));
+    CU(cudaEventRecord(e->ev1, e->stream));
+    double init_s = 0.0;
+    TRY(elapsed(e, &init_s));
+    TRY(fsb_engine_run(e, 0, e->cfg.num_steps, trace, bary, timing));
+    if (timing) timing->seconds_total += init_s;
+    return FSB_OK;
+}
+
+int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
+    TRY(guard(e));
+    if (!e->max_valid) TRY(reduce_current(e));
+    Partial r;
+    TRY(host_combine(e, &r));
+    if (sums) {
+        sums[0] = r.sx;
+        sums[1] = r.sy;
+        sums[2] = r.sf;
+    }
+    if (xy) {
+        xy[0] = r.sx / r.sf;
+        xy[1] = r.sy / r.sf;
+    }
+    return FSB_OK;
+}
+
+int fsb_engine_checksum(fsb_engine* e, uint64_t h_in, uint64_t* h_out) {
+    TRY(guard(e));
+    if (!h_out) return fail(FSB_ERR_INVALID_ARGUMENT, "null h_out");
+    TRY(ensure_staging(e));
+    if (!e->pinned) CU(cudaMallocHost(&e->pinned, kStagingFish * sizeof(fsb_fish)));
+    const fsb_dev::SoA s = canonical(e);
+    uint64_t h = h_in;
+    for (uint64_t lo = 0; lo < e->count; lo += kStagingFish) {
+        const uint64_t cnt = (e->count - lo < kStagingFish) ? e->count - lo : kStagingFish;
+        CU(fsb_dev::launch_soa_to_aos(s, e->cfg.pond_size / 2.0, lo, cnt, e->staging, e->stream));
+        CU(cudaMemcpyAsync(e->pinned, e->staging, cnt * sizeof(fsb_fish), cudaMemcpyDeviceToHost, e->stream));
+        CU(cudaStreamSynchronize(e->stream));
+        h = fsb_checksum_update(h, static_cast<const fsb_fish*>(e->pinned), cnt);
+    }
+    *h_out = h;
+    return FSB_OK;
+}
+
+int fsb_engine_synchronize(fsb_engine* e) {
+    TRY(guard(e));
+    CU(cudaStreamSynchronize(e->stream));
+    return FSB_OK;
+}
+
+int fsb_engine_stream(fsb_engine* e, void** stream) {
+    if (!e || !stream) return fail(FSB_ERR_INVALID_ARGUMENT, "null argument");
+    *stream = e->stream;
+    return FSB_OK;
+}
+
+int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* kernel_ms) {
+    TRY(guard(e));
+    if (!kernel_ms && num_steps) return fail(FSB_ERR_INVALID_ARGUMENT, "null kernel_ms");
+    if (e->count == 0) {
+        for (uint64_t k = 0; k < num_steps; ++k) kernel_ms[k] = 0.0;
+        return FSB_OK;
+    }
+    std::vector<cudaEvent_t> ev(num_steps + 1);
+    for (auto& v : ev) CU(cudaEventCreate(&v));
+    CU(cudaEventRecord(ev[0], e->stream));
+    for (uint64_t k = 0; k < num_steps; ++k) {
+        fsb_dev::StepArgs a = step_args(e, canonical(e));
+        a.step_add = first_step + k;
+        a.part_in = (k == 0) ? nullptr : all_part(e, (int)((k - 1) & 1));
+        a.part_out = local_part(e, (int)(k & 1));
+        CU(fsb_dev::launch_step(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
+        e->cur_explicit = false;
+        CU(cudaEventRecord(ev[k + 1], e->stream));
+        TRY(exchange(e, (int)(k & 1)));
+    }
+    // materialise the last step's eat so the school is a valid end-of-step state
+    if (num_steps) {
+        fsb_dev::EatArgs ea{};
+        ea.s = canonical(e);
+        ea.k = scalars_of(e->cfg);
+        ea.n = e->count;
+        ea.part_in = all_part(e, (int)((num_steps - 1) & 1));
+        ea.world = e->world;
+        CU(fsb_dev::launch_eat(ea, e->grid, e->stream));
+        e->cur_buf = (int)((num_steps - 1) & 1);
+        e->max_valid = true;
+    }
+    CU(cudaStreamSynchronize(e->stream));
+    for (uint64_t k = 0; k < num_steps; ++k) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+        kernel_ms[k] = ms;
+    }
+    for (auto& v : ev) cudaEventDestroy(v);
+    return FSB_OK;
+}
+
+int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches) {
+    if (!e || !launches) return fail(FSB_ERR_INVALID_ARGUMENT, "null argument");
+    *launches = e->last_launches;
+    return FSB_OK;
+}
+
+}  // extern "C"

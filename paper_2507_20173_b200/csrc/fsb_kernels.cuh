@@ -1,0 +1,125 @@
+// fsb_kernels.cuh -- device kernels of the B200 FSB engine and their host
+// launchers (implemented in fsb_kernels.cu, called by fsb_engine.cu).
+//
+// Fish state lives in HBM as structure-of-arrays of fp64:
+//   x[n], y[n], w[n]  position and weight                (Fish::x,y,weight)
+//   p[n]              prev_objective                      (Fish::prev_objective)
+//   c[n]              current_objective -- only materialised after an upload
+//                     whose current_objective is not objective(x, y); in every
+//                     state the engine produces itself cur == objective(x, y)
+//                     bit-for-bit, so it is recomputed instead of stored.
+// One fused step therefore reads 32 B and writes 32 B per fish.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fsb_dev {
+
+constexpr int kThreads = 256;     // threads per CTA of the streaming kernels
+constexpr int kPairsPerThread = 2;  // double2 loads per array per thread per tile
+constexpr int kTilePairs = kThreads * kPairsPerThread;
+constexpr int kTileFish = 2 * kTilePairs;
+
+// Global partials of one step: max(prev-cur) and the barycentre sums
+// sum x*f, sum y*f, sum f.  One per rank; combined in rank order.
+struct alignas(32) Partial {
+    double best;
+    double sx;
+    double sy;
+    double sf;
+};
+
+struct SoA {
+    double* x;
+    double* y;
+    double* w;
+    double* p;
+    double* c;  // nullptr unless current_objective is explicit
+};
+
+struct Scalars {
+    double pond;
+    double half_pond;
+    double step_base;
+    double w_max;
+    uint64_t seed;
+};
+
+// Reduction workspace of one launch.
+struct ReduceWs {
+    Partial* block_part;  // [grid]
+    unsigned* counter;    // zero between launches
+};
+
+struct StepArgs {
+    SoA s;
+    Scalars k;
+    uint64_t n;           // local fish
+    uint64_t gfirst;      // global index of local fish 0 (RNG key, rng.hpp:35)
+    const uint64_t* step_ptr;  // step = (step_ptr ? *step_ptr : 0) + step_add
+    uint64_t step_add;
+    const Partial* part_in;  // [world] previous step's partials, or nullptr (no pending eat)
+    int world;
+    double* trace_out;    // if non-null, CTA 0 stores the previous step's max here
+    double* bary_out;     // if non-null, CTA 0 stores the previous step's 3 sums here
+    ReduceWs ws;
+    Partial* part_out;    // this rank's partial of this step
+    int alternate;        // reverse tile order on odd steps (L2 reuse across steps)
+};
+
+struct EatArgs {
+    SoA s;
+    Scalars k;
+    uint64_t n;
+    const Partial* part_in;
+    int world;
+    double* trace_out;
+    double* bary_out;
+};
+
+struct ReduceArgs {
+    SoA s;
+    Scalars k;
+    uint64_t n;
+    ReduceWs ws;
+    Partial* part_out;
+};
+
+struct InitArgs {
+    SoA s;
+    Scalars k;
+    uint64_t n;
+    uint64_t gfirst;
+    double w0;  // weight_scale
+};
+
+// Small-swarm persistent kernel (one thread-block cluster, state on chip).
+struct ClusterArgs {
+    SoA s;
+    Scalars k;
+    uint64_t n;
+    uint64_t gfirst;
+    uint64_t first_step;
+    uint64_t num_steps;
+    double* trace;        // [num_steps]
+    double* bary;         // [3*num_steps] or nullptr
+    Partial* part_out;    // final step partial (for a later eat())
+};
+
+int step_grid_blocks(int device, bool explicit_cur);
+cudaError_t launch_init(const InitArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_reduce(const ReduceArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_soa_to_aos(const SoA& s, double half_pond, uint64_t lo, uint64_t cnt, void* aos,
+                              cudaStream_t st);
+cudaError_t launch_aos_to_soa(const void* aos, SoA s, double half_pond, uint64_t lo, uint64_t cnt,
+                              int* mismatch, cudaStream_t st);
+cudaError_t launch_copy_cur(SoA s, double half_pond, uint64_t n, cudaStream_t st);
+
+// Cluster kernel: returns cudaErrorNotSupported when n does not fit.
+int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta);
+cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st);
+
+}  // namespace fsb_dev

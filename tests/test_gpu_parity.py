@@ -1,0 +1,285 @@
+"""Parity of the sm_100a engine with the oracle and the reference's golden
+vectors, through the C-ABI.  Requires a B200 (pytest -m gpu).
+
+Bar: bit-exact positions, weights, objectives and max_diff trace (fp64, no
+FMA); barycentre sums within 1e-12 relative of the compensated oracle.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2507_20173_b200 as fsb
+from conftest import ROOT, bits, unhex
+
+pytestmark = pytest.mark.gpu
+
+BARY_RTOL = 1e-12  # north_star: barycentre within 1e-12 relative in fp64
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if fsb.device_count() == 0:
+        pytest.fail("no CUDA device: the GPU tests must run on a B200")
+
+
+def ocfg(cfg: fsb.SimConfig):
+    return oracle.Config.make(num_fish=cfg.num_fish, pond_size=cfg.pond_size,
+                              weight_scale=cfg.weight_scale, num_steps=cfg.num_steps, seed=cfg.seed,
+                              step_base=cfg.step_base)
+
+
+def rel_ok(got, want, rtol=BARY_RTOL):
+    got, want = np.asarray(got), np.asarray(want)
+    return np.all(np.abs(got - want) <= rtol * np.abs(want))
+
+
+STRATS = ["stream", "persistent"]
+
+
+def make(cfg, strategy="auto", **kw):
+    return fsb.Engine(cfg, device=0, strategy=strategy, **kw)
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("name", [
+    "baseline_1000x20", "defaults_10000x100_seed7", "walls_200x50", "band_500x60",
+    "small_500x20_seed42", "one_fish_x30", "ragged_4097x7", "c4_4096x2000",
+])
+def test_golden_runs_every_step(golden_small, golden_states, name, strategy):
+    """Per-step checksum + max_diff of the reference, one run() call per step."""
+    g = golden_small["runs"][name]
+    cfg = fsb.SimConfig(**g["config"])
+    steps = min(cfg.num_steps, 200)
+    with make(cfg, strategy) as eng:
+        eng.init()
+        assert f"{eng.checksum():016x}" == g["init_checksum"]
+        for t in range(steps):
+            trace, _, _ = eng.run(t, 1)
+            assert bits(trace[0]) == g["trace_hex"][t], f"step {t}"
+            assert f"{eng.checksum():016x}" == g["step_checksums"][t], f"step {t}"
+        if steps < cfg.num_steps:
+            trace, _, _ = eng.run(steps, cfg.num_steps - steps)
+            assert [bits(v) for v in trace] == g["trace_hex"][steps:]
+        assert f"{eng.checksum():016x}" == g["step_checksums"][-1]
+        if name + "__final" in golden_states:
+            assert eng.download().tobytes() == golden_states[name + "__final"].tobytes()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("alternate", [True, False])
+@pytest.mark.parametrize("n,t", [(1, 9), (2, 9), (3, 9), (31, 9), (33, 9), (255, 7), (1025, 7),
+                                 (2 * 1024 + 1, 6), (12289, 5), (16384, 5), (65536, 3)])
+def test_sizes_bit_exact(orc, n, t, strategy, alternate):
+    cfg = fsb.baseline_config(n, t)
+    if strategy == "persistent" and n > 65536:
+        pytest.skip("above the persistent capacity")
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, strategy, alternate=alternate) as eng:
+        trace, bary, _ = eng.simulate(barycentre=True)
+        got = eng.download()
+    assert got.tobytes() == want_fish.tobytes()
+    assert trace.tobytes() == want_trace.tobytes()
+    assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_per_step_barycentre(orc, strategy):
+    cfg = fsb.SimConfig(num_fish=12000, pond_size=50.0, weight_scale=2.0, num_steps=12, seed=99,
+                        step_base=0.9)
+    fish = orc.init(ocfg(cfg))
+    want = []
+    for t in range(cfg.num_steps):
+        orc.move(ocfg(cfg), t, fish)
+        orc.eat(ocfg(cfg), fish)
+        want.append(orc.barycentre_sums(fish))
+    with make(cfg, strategy) as eng:
+        _, bary, _ = eng.simulate(barycentre=True)
+        sums, xy = eng.barycentre()
+    assert rel_ok(bary, np.array(want))
+    assert rel_ok(sums, want[-1])
+    assert rel_ok(xy, [want[-1][0] / want[-1][2], want[-1][1] / want[-1][2]], 1e-12)
+
+
+def test_large_stream_bit_exact(orc):
+    cfg = fsb.SimConfig(num_fish=1_000_003, pond_size=200.0, weight_scale=10.0, num_steps=25, seed=7,
+                        step_base=1.0)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "stream") as eng:
+        trace, bary, _ = eng.simulate(barycentre=True)
+        got = eng.download()
+    assert got.tobytes() == want_fish.tobytes()
+    assert trace.tobytes() == want_trace.tobytes()
+    assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
+
+
+def test_phase_api_move_then_eat(orc):
+    """move_phase / eat_phase as separate calls: the state after each phase."""
+    cfg = fsb.SimConfig(num_fish=5001, num_steps=6, seed=3)
+    oc = ocfg(cfg)
+    fish = orc.init(oc)
+    with make(cfg) as eng:
+        eng.init()
+        for t in range(cfg.num_steps):
+            orc.move(oc, t, fish)
+            eng.move(t)
+            assert eng.download().tobytes() == fish.tobytes(), f"after move {t}"
+            m = orc.eat(oc, fish)
+            r = eng.eat()
+            assert bits(r.max_diff) == bits(m)
+            assert eng.download().tobytes() == fish.tobytes(), f"after eat {t}"
+
+
+def test_host_school_phase_functions(orc):
+    """The reference call shapes on a host School (sim.hpp:84,110)."""
+    cfg = fsb.SimConfig(num_fish=700, num_steps=5, seed=11)
+    oc = ocfg(cfg)
+    ex = fsb.GpuExecutor()
+    school = fsb.init_school(cfg, ex)
+    want = orc.init(oc)
+    assert school.fishes.tobytes() == want.tobytes()
+    for t in range(cfg.num_steps):
+        fsb.move_phase(school, cfg, t, ex)
+        r = fsb.eat_phase(school, cfg, ex)
+        orc.move(oc, t, want)
+        assert bits(r.max_diff) == bits(orc.eat(oc, want))
+        assert school.fishes.tobytes() == want.tobytes()
+    res = fsb.simulate(cfg, ex)
+    assert fsb.checksum(res.school) == fsb.checksum(school)
+    ex.close()
+
+
+def test_eat_examples_from_reference_tests(golden_small):
+    """test_sim.cpp:139-191 hand-built schools (current_objective != objective(x,y))."""
+    cfg = fsb.SimConfig()
+    ex = fsb.GpuExecutor()
+    for name, case in golden_small["eat_examples"].items():
+        rows = [tuple(unhex(v) for v in r) for r in case["input"]]
+        school = fsb.School(np.array(rows, dtype=fsb.FISH_DTYPE) if rows else None)
+        r = fsb.eat_phase(school, cfg, ex)
+        assert bits(r.max_diff) == case["max_diff"], name
+        assert [bits(w) for w in school.fishes["weight"]] == case["weights"], name
+        # x, y, prev, cur untouched
+        for k, fld in enumerate(("x", "y")):
+            assert [bits(v) for v in school.fishes[fld]] == [r_[k] for r_ in case["input"]]
+    ex.close()
+
+
+@pytest.mark.parametrize("strategy", STRATS)
+def test_upload_inconsistent_then_run(orc, strategy):
+    """An uploaded school whose current_objective is arbitrary (explicit-cur path)."""
+    rng = np.random.default_rng(5)
+    n = 3001
+    fish = np.zeros(n, dtype=oracle.FISH_DTYPE)
+    fish["x"] = rng.uniform(0, 200, n)
+    fish["y"] = rng.uniform(0, 200, n)
+    fish["weight"] = rng.uniform(1, 20, n)
+    fish["prev_objective"] = rng.uniform(0, 150, n)
+    fish["current_objective"] = rng.uniform(0, 150, n)
+    cfg = fsb.SimConfig(num_fish=n, num_steps=4, seed=17)
+    oc = ocfg(cfg)
+    with make(cfg, strategy) as eng:
+        eng.upload(fish)
+        assert eng.download().tobytes() == fish.tobytes()
+        want = fish.copy()
+        m = orc.eat(oc, want)  # eat first (uses the explicit cur)
+        assert bits(eng.eat().max_diff) == bits(m)
+        assert eng.download().tobytes() == want.tobytes()
+        trace, _, _ = eng.run(0, 4)
+        want_trace = orc.run(oc, want, 0, 4)
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == want.tobytes()
+    with make(cfg, strategy) as eng:  # run straight after the upload
+        eng.upload(fish)
+        want = fish.copy()
+        trace, _, _ = eng.run(0, 4)
+        assert trace.tobytes() == orc.run(oc, want, 0, 4).tobytes()
+        assert eng.download().tobytes() == want.tobytes()
+
+
+def test_run_split_equals_whole(orc):
+    cfg = fsb.baseline_config(40_000, 12)
+    with make(cfg, "stream") as a, make(cfg, "stream") as b:
+        a.init()
+        b.init()
+        ta, _, _ = a.run(0, 12)
+        tb1, _, _ = b.run(0, 5)
+        tb2, _, _ = b.run(5, 7)
+        tb3, _, _ = b.run(12, 0)
+        assert ta.tobytes() == np.concatenate([tb1, tb2, tb3]).tobytes()
+        assert a.download().tobytes() == b.download().tobytes()
+
+
+def test_empty_school():
+    cfg = fsb.SimConfig(num_fish=0, num_steps=4)
+    with make(cfg) as eng:
+        eng.init()
+        trace, bary, _ = eng.run(0, 4, barycentre=True)
+        assert np.all(trace == -np.inf)
+        assert eng.eat().max_diff == -np.inf
+        assert eng.checksum() == fsb.kChecksumEmpty
+        assert eng.download().shape == (0,)
+
+
+def test_repeatable_bitwise():
+    cfg = fsb.baseline_config(300_001, 10)
+    outs = []
+    for _ in range(2):
+        with make(cfg, "stream") as eng:
+            trace, bary, _ = eng.simulate(barycentre=True)
+            outs.append((trace.tobytes(), bary.tobytes(), eng.checksum()))
+    assert outs[0] == outs[1]
+
+
+def test_time_step_kernels_keeps_state_valid(orc):
+    cfg = fsb.baseline_config(200_000, 6)
+    fish = orc.init(ocfg(cfg))
+    orc.run(ocfg(cfg), fish, 0, 6)
+    with make(cfg, "stream") as eng:
+        eng.init()
+        ms = eng.time_step_kernels(0, 6)
+        assert ms.shape == (6,) and np.all(ms > 0)
+        assert eng.download().tobytes() == fish.tobytes()
+
+
+def test_force_nccl_world1(orc):
+    """The NCCL exchange path (allgather in the graph) on one rank."""
+    cfg = fsb.baseline_config(100_000, 8)
+    uid = fsb.nccl_unique_id()
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "stream", nccl_unique_id=uid, force_nccl=True) as eng:
+        trace, _, _ = eng.simulate(barycentre=False)
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == want_fish.tobytes()
+        eng.move(8)
+        orc.move(ocfg(cfg), 8, want_fish)
+        assert bits(eng.eat().max_diff) == bits(orc.eat(ocfg(cfg), want_fish))
+
+
+@pytest.mark.parametrize("name", ["C0_1e6x100", "C1_1e7x100", "C4_4096x100000", "C2_1e8x50"])
+def test_baseline_configs_match_reference_digests(golden_baseline, orc, name):
+    if name not in golden_baseline:
+        pytest.skip("digest not generated")
+    g = golden_baseline[name]
+    cfg = fsb.SimConfig(**g["config"])
+    with make(cfg) as eng:
+        trace, bary, _ = eng.simulate(barycentre=True)
+        assert f"{eng.checksum():016x}" == g["final_checksum"]
+    assert bits(trace[-1]) == g["trace_last_hex"]
+    if g.get("trace_hex"):
+        assert [bits(v) for v in trace] == g["trace_hex"]
+    if g.get("trace_every_1000_hex"):
+        assert [bits(v) for v in trace[999::1000]] == g["trace_every_1000_hex"]
+    assert rel_ok(bary[-1], [unhex(v) for v in g["barycentre_fsum"]])
+
+
+def test_cpp_dropin_suite():
+    """tests/cpp/test_gpu_sim: the reference's test_sim.cpp cases via fsb::gpu."""
+    exe = os.path.join(ROOT, "tests", "cpp", "test_gpu_sim")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.dirname(exe)], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
