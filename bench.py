@@ -245,7 +245,7 @@ def run_ours(args, world, rank, local):
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     eng = fsb.Engine(cfg, device=local, rank=rank, world_size=world, nccl_unique_id=uid,
-                     strategy=args.strategy)
+                     strategy=args.strategy, alternate=not args.no_alternate)
     eng.init()
     if args.warmup:
         eng.run(0, args.warmup)
@@ -352,6 +352,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--fish", type=int, default=FISH_PER_GPU, help="fish per GPU")
     ap.add_argument("--strategy", default="auto", choices=["auto", "stream", "persistent"])
+    ap.add_argument("--no-alternate", action="store_true",
+                    help="fixed tile order (default reverses odd steps to reuse L2 across steps)")
     ap.add_argument("--cpu-steps", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

@@ -262,10 +262,35 @@ __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
     const double M = prev.best;
     if (!(M > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
     const double half = a.k.half_pond;
+    const double w_max = a.k.w_max;
+    const uint64_t npairs = a.n >> 1;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const double2* X2 = reinterpret_cast<const double2*>(a.s.x);
+    const double2* Y2 = reinterpret_cast<const double2*>(a.s.y);
+    const double2* P2 = reinterpret_cast<const double2*>(a.s.p);
+    const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
+    double2* W2 = reinterpret_cast<double2*>(a.s.w);
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
+        double2 W = W2[q];
+        const double2 P = P2[q];
+        double c0, c1;
+        if (kExplicitCur) {
+            const double2 C = C2[q];
+            c0 = C.x;
+            c1 = C.y;
+        } else {
+            const double2 X = X2[q], Y = Y2[q];
+            c0 = objective(X.x, Y.x, half);
+            c1 = objective(X.y, Y.y, half);
+        }
+        W.x = eat_weight(W.x, P.x, c0, M, w_max);
+        W.y = eat_weight(W.y, P.y, c1, M, w_max);
+        W2[q] = W;
+    }
+    if ((a.n & 1ull) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t i = a.n - 1;
         const double cur = kExplicitCur ? a.s.c[i] : objective(a.s.x[i], a.s.y[i], half);
-        a.s.w[i] = eat_weight(a.s.w[i], a.s.p[i], cur, M, a.k.w_max);
+        a.s.w[i] = eat_weight(a.s.w[i], a.s.p[i], cur, M, w_max);
     }
 }
 
@@ -327,7 +352,7 @@ __global__ void aos_to_soa_kernel(const FishAoS* in, SoA s, double half, uint64_
 constexpr int kMaxCluster = 16;
 
 template <int F>
-__global__ void __launch_bounds__(1024 / F) cluster_kernel(const ClusterArgs a) {
+__global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned crank = cluster.block_rank();
     const unsigned ncta = cluster.num_blocks();
@@ -494,12 +519,11 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
     if (!cached) {
         cudaFuncSetAttribute(cluster_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(cluster_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(cluster_kernel<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cached = 8;
         for (int c : {16, 8}) {
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(c);
-            cfg.blockDim = dim3(256);
+            cfg.blockDim = dim3(1024);
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
             attr[0].val.clusterDim.x = c;
@@ -508,7 +532,7 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<4>, &cfg) == cudaSuccess &&
+            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<2>, &cfg) == cudaSuccess &&
                 nclusters >= 1) {
                 cached = c;
                 break;
@@ -518,7 +542,7 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
     }
     if (cluster_ctas) *cluster_ctas = cached;
     if (threads_per_cta) *threads_per_cta = 256;
-    return cached * 4096;  // 4096 fish per CTA at most (256 threads x 4 fish)
+    return cached * 2048;  // 2048 fish per CTA at most (1024 threads x 2 fish)
 }
 
 cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
@@ -528,13 +552,13 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     const int capacity = cluster_capacity(dev, &cmax, nullptr);
     if (a.n == 0 || a.n > (uint64_t)capacity) return cudaErrorNotSupported;
     // ~256 fish per CTA, at most cmax CTAs; F fish per thread with F*threads
-    // <= 1024 (the register budget of __launch_bounds__(1024 / F)).
+    // <= 1024 threads; F = 2 still fits the 64-register budget without spills.
     uint64_t ncta = (a.n + 255) / 256;
     if (ncta > (uint64_t)cmax) ncta = cmax;
     if (ncta < 1) ncta = 1;
     const uint64_t per_cta = (a.n + ncta - 1) / ncta;
-    uint64_t fpt = per_cta <= 1024 ? 1 : (per_cta <= 2048 ? 2 : 4);
-    if (per_cta > 4096) return cudaErrorNotSupported;
+    const uint64_t fpt = per_cta <= 1024 ? 1 : 2;
+    if (per_cta > 2048) return cudaErrorNotSupported;
     const uint64_t threads = (((per_cta + fpt - 1) / fpt + 31) / 32) * 32;
 
     cudaLaunchConfig_t cfg = {};
@@ -549,8 +573,7 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (fpt == 1) return cudaLaunchKernelEx(&cfg, cluster_kernel<1>, a);
-    if (fpt == 2) return cudaLaunchKernelEx(&cfg, cluster_kernel<2>, a);
-    return cudaLaunchKernelEx(&cfg, cluster_kernel<4>, a);
+    return cudaLaunchKernelEx(&cfg, cluster_kernel<2>, a);
 }
 
 }  // namespace fsb_dev
