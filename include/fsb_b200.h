@@ -76,6 +76,7 @@ enum fsb_strategy {
 /* Engine flags. */
 #define FSB_FLAG_NO_ALTERNATE 0x1u /* keep tile order fixed (default reverses odd steps for L2 reuse) */
 #define FSB_FLAG_FORCE_NCCL 0x2u   /* use the NCCL exchange even when world_size == 1 (testing) */
+#define FSB_FLAG_NO_BULK 0x4u      /* step kernel loads with LDG instead of the cp.async.bulk smem ring */
 
 typedef struct fsb_engine_options {
     int device;                  /* CUDA device ordinal of this shard */
@@ -166,6 +167,13 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
 
 /* Kernel launch count of the last fsb_engine_run (for bench accounting). */
 int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches);
+
+/* Device self-test of the guarded fast fp64 paths the step kernel uses
+ * (fsb_math.cuh): n generated operands (raw bit patterns incl. NaN, inf,
+ * subnormals, and the simulation's value ranges).  out[0..2] = bitwise
+ * mismatches vs __ddiv_rn (hoisted divisor), __ddiv_rn (per operand) and
+ * __dsqrt_rn; out[3] = guard failures on simulation-range operands. */
+int fsb_selftest_fast_math(int device, uint64_t n, uint64_t seed, uint64_t out[4]);
 
 #ifdef __cplusplus
 }

@@ -25,6 +25,7 @@ STRATEGY_PERSISTENT = 2
 
 FLAG_NO_ALTERNATE = 0x1
 FLAG_FORCE_NCCL = 0x2
+FLAG_NO_BULK = 0x4
 
 
 class fsb_sim_config(ctypes.Structure):
@@ -86,6 +87,7 @@ SIGNATURES = [
     ("fsb_engine_stream", _int, [_vp, _P(_vp)]),
     ("fsb_engine_time_step_kernels", _int, [_vp, _u64, _u64, _vp]),
     ("fsb_engine_last_launches", _int, [_vp, _P(_u64)]),
+    ("fsb_selftest_fast_math", _int, [_int, _u64, _u64, _vp]),
 ]
 
 
@@ -99,10 +101,11 @@ _lib = None
 
 
 def lib() -> ctypes.CDLL:
-    """Load (building first if stale) libfsb_b200.so."""
+    """Load (building first if stale) libfsb_b200.so.  FSB_LIB may name a
+    prebuilt variant of the same library (tools/variants.py A/B builds)."""
     global _lib
     if _lib is None:
-        path = _build.build()
+        path = os.environ.get("FSB_LIB") or _build.build()
         L = ctypes.CDLL(path)
         for name, res, args in SIGNATURES:
             fn = getattr(L, name)
@@ -115,7 +118,7 @@ def lib() -> ctypes.CDLL:
 
 
 def lib_path() -> str:
-    return os.path.abspath(_build.LIB)
+    return os.path.abspath(os.environ.get("FSB_LIB") or _build.LIB)
 
 
 def check(rc: int) -> None:

@@ -222,6 +222,7 @@ fsb_dev::StepArgs step_args(fsb_engine* e, const fsb_dev::SoA& s) {
     a.ws.block_part = e->block_part;
     a.ws.counter = e->counter;
     a.alternate = (e->flags & FSB_FLAG_NO_ALTERNATE) ? 0 : 1;
+    a.bulk = (e->flags & FSB_FLAG_NO_BULK) ? 0 : 1;
     return a;
 }
 
@@ -528,8 +529,8 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     CB(cudaMalloc(&e->s.w, bytes));
     CB(cudaMalloc(&e->s.p, bytes));
     e->s.c = nullptr;
-    e->grid = fsb_dev::step_grid_blocks(e->device, false);
-    e->grid_explicit = fsb_dev::step_grid_blocks(e->device, true);
+    e->grid = fsb_dev::step_grid_blocks(e->device, false, !(e->flags & FSB_FLAG_NO_BULK));
+    e->grid_explicit = fsb_dev::step_grid_blocks(e->device, true, false);
     const int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
@@ -798,3 +799,23 @@ int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches) {
 }
 
 }  // extern "C"
+
+extern "C" int fsb_selftest_fast_math(int device, uint64_t n, uint64_t seed, uint64_t out[4]) {
+    if (!out) return fail(FSB_ERR_INVALID_ARGUMENT, "null out");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(FSB_ERR_CUDA, "no CUDA device available");
+    }
+    CU(cudaSetDevice(device));
+    unsigned long long* d = nullptr;
+    CU(cudaMalloc(&d, 4 * sizeof *d));
+    cudaError_t e = cudaMemset(d, 0, 4 * sizeof *d);
+    if (e == cudaSuccess) e = fsb_dev::launch_selftest_fast_math(n, seed, d, 0);
+    unsigned long long h[4] = {0, 0, 0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "selftest fast math");
+    for (int k = 0; k < 4; ++k) out[k] = h[k];
+    return FSB_OK;
+}

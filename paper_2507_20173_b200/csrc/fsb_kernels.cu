@@ -108,7 +108,7 @@ __device__ __forceinline__ void store_partial(Partial* p, const Partial& v) {
 // CTA partial -> global; the last CTA to arrive combines all CTA partials in
 // index order and publishes this rank's partial.
 __device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs& ws, Partial* part_out) {
-    __shared__ Partial scratch[kThreads / 32];
+    __shared__ Partial scratch[32];
     __shared__ bool am_last;
     const Partial blk = block_reduce(local, scratch);
     if (threadIdx.x == 0) {
@@ -163,12 +163,102 @@ __device__ __forceinline__ StepParams params_of(const Scalars& k) {
 // One fish of the fused step.  cur is this fish's current objective before
 // the step (recomputed or explicit).  Returns nothing; updates state + acc.
 __device__ __forceinline__ void fused_fish(double& x, double& y, double& w, double& p, double cur,
-                                           bool eat, double M, uint64_t gi, uint64_t step,
-                                           const StepParams& P, Partial& acc) {
+                                           bool eat, const SharedDivisor& M, uint64_t gi,
+                                           uint64_t step, const StepParams& P, Partial& acc) {
     if (eat) w = eat_weight(w, p, cur, M, P.w_max);          // sim.hpp:115-120 (step-1)
     const double cn = swim(x, y, w, fold_in(P.seed, gi), step, P);  // sim.hpp:90-97
     p = cur;                                                   // sim.hpp:96
     accumulate(acc, x, y, cur, cn);                            // sim.hpp:112-114
+}
+
+// The same fish update on the guarded fast paths: returns the new objective
+// and ANDs the operand guards into ok (no accumulation: the caller folds the
+// fish into its partial once the result is final).
+__device__ __forceinline__ double fused_fish_guarded(double& x, double& y, double& w, double& p,
+                                                     double cur, bool eat, const SharedDivisor& M,
+                                                     uint64_t gi, uint64_t step, const StepParams& P,
+                                                     bool& ok) {
+    if (eat) w = eat_weight_guarded(w, p, cur, M, P.w_max, ok);
+    const double cn = swim_guarded(x, y, w, fold_in(P.seed, gi), step, P, ok);
+    p = cur;
+    return cn;
+}
+
+// ... and on the exact intrinsics (the fallback for a failed guard; kept out
+// of line so the hot loop carries none of its registers).
+struct FishOut {
+    double x, y, w, p, cn;
+};
+
+__device__ __noinline__ FishOut fused_fish_exact(double x, double y, double w, double p, double cur,
+                                                 bool eat, double M, uint64_t gi, uint64_t step,
+                                                 StepParams P) {
+    if (eat) w = eat_weight(w, p, cur, M, P.w_max);
+    const double cn = swim(x, y, w, fold_in(P.seed, gi), step, P);
+    return FishOut{x, y, w, cur, cn};
+}
+
+// Where a pair's original state can be re-read (global SoA or a smem stage).
+struct SoA2 {
+    const double2* x;
+    const double2* y;
+    const double2* w;
+    const double2* p;
+    const double2* c;
+};
+
+// U pairs of fish through the fused step.  X..Q hold each pair's state on
+// entry and the new state on exit; pair u is fish gi[u], gi[u]+1 and can be
+// re-read from src at index k[u].  All 2U fish run their guarded fast paths
+// first (independent chains the scheduler interleaves), then ONE warp vote:
+// a pair whose guard failed is recomputed with the exact intrinsics.  Only
+// then are the fish folded into the thread partial.
+template <bool kExplicitCur, int U>
+__device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], double2 (&W)[U],
+                                            double2 (&Q)[U], const double2 (&C)[U], const bool (&valid)[U],
+                                            const SoA2& src, const uint64_t (&k)[U], const uint64_t (&gi)[U],
+                                            const StepParams& P, bool eat, const SharedDivisor& M,
+                                            uint64_t step, Partial& acc) {
+    bool ok[U];
+    double n0[U], n1[U];
+    bool all_ok = true;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        ok[u] = true;
+        if (valid[u]) {
+            const double c0 = kExplicitCur ? C[u].x : objective_guarded(X[u].x, Y[u].x, P.half_pond, ok[u]);
+            const double c1 = kExplicitCur ? C[u].y : objective_guarded(X[u].y, Y[u].y, P.half_pond, ok[u]);
+            n0[u] = fused_fish_guarded(X[u].x, Y[u].x, W[u].x, Q[u].x, c0, eat, M, gi[u], step, P, ok[u]);
+            n1[u] = fused_fish_guarded(X[u].y, Y[u].y, W[u].y, Q[u].y, c1, eat, M, gi[u] + 1, step, P, ok[u]);
+            all_ok &= ok[u];
+        }
+    }
+    if (__any_sync(__activemask(), !all_ok)) {  // never taken for in-range simulation values
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (valid[u] && !ok[u]) {
+                const uint64_t j = k[u];
+                const double2 x0 = src.x[j], y0 = src.y[j], w0 = src.w[j], p0 = src.p[j];
+                const double e0 = kExplicitCur ? src.c[j].x : objective(x0.x, y0.x, P.half_pond);
+                const double e1 = kExplicitCur ? src.c[j].y : objective(x0.y, y0.y, P.half_pond);
+                const FishOut f0 = fused_fish_exact(x0.x, y0.x, w0.x, p0.x, e0, eat, M.b, gi[u], step, P);
+                const FishOut f1 = fused_fish_exact(x0.y, y0.y, w0.y, p0.y, e1, eat, M.b, gi[u] + 1, step, P);
+                X[u] = make_double2(f0.x, f1.x);
+                Y[u] = make_double2(f0.y, f1.y);
+                W[u] = make_double2(f0.w, f1.w);
+                Q[u] = make_double2(f0.p, f1.p);
+                n0[u] = f0.cn;
+                n1[u] = f1.cn;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (valid[u]) {
+            accumulate(acc, X[u].x, Y[u].x, Q[u].x, n0[u]);
+            accumulate(acc, X[u].y, Y[u].y, Q[u].y, n1[u]);
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -190,18 +280,28 @@ __global__ void __launch_bounds__(kThreads) init_kernel(const InitArgs a) {
 }
 
 template <bool kExplicitCur>
-__global__ void __launch_bounds__(kThreads) step_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
     const StepParams P = params_of(a.k);
     const Partial prev = combine_ranks(a.part_in, a.world);
     publish_prev(prev, a.trace_out, a.bary_out);
-    const double M = prev.best;
-    const bool eat = M > 0.0;  // sim.hpp:115
+    const bool eat = prev.best > 0.0;  // sim.hpp:115
+    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
 
     const uint64_t n = a.n;
     const uint64_t npairs = n >> 1;
-    const uint64_t ntiles = (npairs + kTilePairs - 1) / kTilePairs;
     const bool rev = a.alternate && (step & 1ull);
+
+    // Each CTA owns one balanced contiguous chunk of pairs (boundaries aligned
+    // to 64 pairs = 1 KB per array), walked in sub-tiles of kTilePairs.  Odd
+    // steps walk it backwards, so the sub-tiles a CTA touched last in step t
+    // (still in L2) are the first it reads in step t+1.
+    constexpr uint64_t kAlign = 64;
+    const uint64_t nblk = (npairs + kAlign - 1) / kAlign;
+    const uint64_t lo = (nblk * blockIdx.x / gridDim.x) * kAlign;
+    uint64_t hi = (nblk * (blockIdx.x + 1) / gridDim.x) * kAlign;
+    if (hi > npairs) hi = npairs;
+    const uint64_t nsub = hi > lo ? (hi - lo + kTilePairs - 1) / kTilePairs : 0;
 
     double2* X2 = reinterpret_cast<double2*>(a.s.x);
     double2* Y2 = reinterpret_cast<double2*>(a.s.y);
@@ -210,15 +310,21 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const StepArgs a) {
     const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
 
     Partial acc = identity();
-    for (uint64_t it = blockIdx.x; it < ntiles; it += gridDim.x) {
-        const uint64_t tile = rev ? ntiles - 1 - it : it;
-        const uint64_t base = tile * kTilePairs + threadIdx.x;
+    for (uint64_t j = 0; j < nsub; ++j) {
+        const uint64_t sub = rev ? nsub - 1 - j : j;
+        const uint64_t base = lo + sub * kTilePairs + threadIdx.x;
         double2 X[kPairsPerThread], Y[kPairsPerThread], W[kPairsPerThread], Q[kPairsPerThread],
             C[kPairsPerThread];
+        bool valid[kPairsPerThread];
+        uint64_t qs[kPairsPerThread], gi[kPairsPerThread];
 #pragma unroll
         for (int u = 0; u < kPairsPerThread; ++u) {
-            const uint64_t q = base + (uint64_t)u * kThreads;
-            if (q < npairs) {
+            const uint64_t qq = base + (uint64_t)u * kThreads;
+            const uint64_t q = FSB_MEM_WINDOW ? lo + ((qq - lo) % FSB_MEM_WINDOW) : qq;
+            qs[u] = q;
+            gi[u] = a.gfirst + 2 * qq;
+            valid[u] = qq < hi;
+            if (valid[u]) {
                 X[u] = X2[q];
                 Y[u] = Y2[q];
                 W[u] = W2[q];
@@ -226,15 +332,12 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const StepArgs a) {
                 if (kExplicitCur) C[u] = C2[q];
             }
         }
+        const SoA2 src{X2, Y2, W2, P2, C2};
+        fused_pairs<kExplicitCur, kPairsPerThread>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
 #pragma unroll
         for (int u = 0; u < kPairsPerThread; ++u) {
-            const uint64_t q = base + (uint64_t)u * kThreads;
-            if (q < npairs) {
-                const uint64_t gi = a.gfirst + 2 * q;
-                const double c0 = kExplicitCur ? C[u].x : objective(X[u].x, Y[u].x, P.half_pond);
-                const double c1 = kExplicitCur ? C[u].y : objective(X[u].y, Y[u].y, P.half_pond);
-                fused_fish(X[u].x, Y[u].x, W[u].x, Q[u].x, c0, eat, M, gi, step, P, acc);
-                fused_fish(X[u].y, Y[u].y, W[u].y, Q[u].y, c1, eat, M, gi + 1, step, P, acc);
+            const uint64_t q = qs[u];
+            if (valid[u]) {
                 X2[q] = X[u];
                 Y2[q] = Y[u];
                 W2[q] = W[u];
@@ -255,12 +358,198 @@ __global__ void __launch_bounds__(kThreads) step_kernel(const StepArgs a) {
     grid_finish(acc, a.ws, a.part_out);
 }
 
+// ---------------------------------------------------------------------------
+// step_kernel_bulk: the same fused step with the state streamed HBM -> shared
+// memory by the bulk-copy engine (cp.async.bulk, the 1-D TMA path) through a
+// kBulkStages-deep ring of sub-tiles, completion tracked by mbarriers.  Thread
+// 0 keeps the ring full; every thread computes one pair per sub-tile from
+// shared memory and stores the new state straight to HBM.  Loads in flight no
+// longer occupy registers, so memory latency is hidden by the ring instead of
+// by warps.  Compact state only (the explicit-cur step uses step_kernel).
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "FSB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra FSB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+struct BulkStage {
+    double2 x[kBulkTilePairs];
+    double2 y[kBulkTilePairs];
+    double2 w[kBulkTilePairs];
+    double2 p[kBulkTilePairs];
+};
+
+// Warps 0..7 compute (kBulkPairsPerThread pairs each per sub-tile); warp 8 is
+// the producer whose elected lane keeps the ring full.
+__global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel_bulk(const StepArgs a) {
+    extern __shared__ __align__(128) unsigned char bulk_smem[];
+    BulkStage* stage = reinterpret_cast<BulkStage*>(bulk_smem);
+    __shared__ __align__(8) uint64_t full[kBulkStages];
+    __shared__ __align__(8) uint64_t empty[kBulkStages];
+
+    const StepParams P = params_of(a.k);
+    const Partial prev = combine_ranks(a.part_in, a.world);
+    publish_prev(prev, a.trace_out, a.bary_out);
+    const bool eat = prev.best > 0.0;  // sim.hpp:115
+    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
+    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
+    const uint64_t n = a.n;
+    const uint64_t npairs = n >> 1;
+    const bool rev = a.alternate && (step & 1ull);
+
+    constexpr uint64_t kAlign = 64;  // balanced chunk per CTA, as in step_kernel
+    const uint64_t nblk = (npairs + kAlign - 1) / kAlign;
+    const uint64_t lo = (nblk * blockIdx.x / gridDim.x) * kAlign;
+    uint64_t hi = (nblk * (blockIdx.x + 1) / gridDim.x) * kAlign;
+    if (hi > npairs) hi = npairs;
+    const uint64_t nsub = hi > lo ? (hi - lo + kBulkTilePairs - 1) / kBulkTilePairs : 0;
+
+    double2* X2 = reinterpret_cast<double2*>(a.s.x);
+    double2* Y2 = reinterpret_cast<double2*>(a.s.y);
+    double2* W2 = reinterpret_cast<double2*>(a.s.w);
+    double2* P2 = reinterpret_cast<double2*>(a.s.p);
+
+    const unsigned t = threadIdx.x;
+    if (t == 0) {
+        for (int s = 0; s < kBulkStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kBulkCompute / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto sub_base = [&](uint64_t j) { return lo + (rev ? nsub - 1 - j : j) * (uint64_t)kBulkTilePairs; };
+    Partial acc = identity();
+    if (t >= kBulkCompute) {
+        // Producer warp, elected lane.  Sub-tile j lives in stage j % kBulkStages:
+        // bulk-load it; once the compute warps have written its new state back
+        // into the stage (empty[s]), bulk-store the stage to HBM and, as soon as
+        // the store has read the stage out, reuse it for sub-tile j + kBulkStages.
+        if (t == kBulkCompute) {
+            auto load = [&](uint64_t j) {
+                const int s = (int)(j % kBulkStages);
+                const uint64_t base = sub_base(j);
+                const uint64_t cnt = (hi - base < (uint64_t)kBulkTilePairs) ? hi - base : (uint64_t)kBulkTilePairs;
+                const unsigned bytes = (unsigned)(cnt * sizeof(double2));
+                mbar_expect_tx(&full[s], 4 * bytes);
+                bulk_load(stage[s].x, X2 + base, bytes, &full[s]);
+                bulk_load(stage[s].y, Y2 + base, bytes, &full[s]);
+                bulk_load(stage[s].w, W2 + base, bytes, &full[s]);
+                bulk_load(stage[s].p, P2 + base, bytes, &full[s]);
+            };
+            for (uint64_t j = 0; j < nsub && j < (uint64_t)kBulkStages; ++j) load(j);
+            for (uint64_t j = 0; j < nsub; ++j) {
+                const int s = (int)(j % kBulkStages);
+                mbar_wait(&empty[s], (unsigned)((j / kBulkStages) & 1));
+                const uint64_t base = sub_base(j);
+                const uint64_t cnt = (hi - base < (uint64_t)kBulkTilePairs) ? hi - base : (uint64_t)kBulkTilePairs;
+                const unsigned bytes = (unsigned)(cnt * sizeof(double2));
+                bulk_store(X2 + base, stage[s].x, bytes);
+                bulk_store(Y2 + base, stage[s].y, bytes);
+                bulk_store(W2 + base, stage[s].w, bytes);
+                bulk_store(P2 + base, stage[s].p, bytes);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                if (j + kBulkStages < nsub) {
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    load(j + kBulkStages);
+                }
+            }
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
+        }
+    } else {
+        for (uint64_t j = 0; j < nsub; ++j) {
+            const int s = (int)(j % kBulkStages);
+            const uint64_t base = sub_base(j);
+            mbar_wait(&full[s], (unsigned)((j / kBulkStages) & 1));
+            const SoA2 src{stage[s].x, stage[s].y, stage[s].w, stage[s].p, nullptr};
+            double2 X[kBulkPairsPerThread], Y[kBulkPairsPerThread], W[kBulkPairsPerThread], Q[kBulkPairsPerThread];
+            bool valid[kBulkPairsPerThread];
+            uint64_t ks[kBulkPairsPerThread], gi[kBulkPairsPerThread];
+#pragma unroll
+            for (int u = 0; u < kBulkPairsPerThread; ++u) {
+                const unsigned k = t + u * kBulkCompute;
+                ks[u] = k;
+                gi[u] = a.gfirst + 2 * (base + k);
+                valid[u] = base + k < hi;
+                if (valid[u]) {
+                    X[u] = stage[s].x[k];
+                    Y[u] = stage[s].y[k];
+                    W[u] = stage[s].w[k];
+                    Q[u] = stage[s].p[k];
+                }
+            }
+            fused_pairs<false, kBulkPairsPerThread>(X, Y, W, Q, X, valid, src, ks, gi, P, eat, M, step, acc);
+#pragma unroll
+            for (int u = 0; u < kBulkPairsPerThread; ++u) {  // new state back into the stage
+                const unsigned k = (unsigned)ks[u];
+                if (valid[u]) {
+                    stage[s].x[k] = X[u];
+                    stage[s].y[k] = Y[u];
+                    stage[s].w[k] = W[u];
+                    stage[s].p[k] = Q[u];
+                }
+            }
+            // make the generic-proxy smem writes visible to the bulk-store (async) proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if ((t & 31) == 0) mbar_arrive(&empty[s]);
+        }
+        if ((n & 1ull) && blockIdx.x == 0 && t == 0) {  // odd tail fish
+            const uint64_t i = n - 1;
+            double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];
+            fused_fish(x, y, w, p, objective(x, y, P.half_pond), eat, M, a.gfirst + i, step, P, acc);
+            a.s.x[i] = x;
+            a.s.y[i] = y;
+            a.s.w[i] = w;
+            a.s.p[i] = p;
+        }
+    }
+    grid_finish(acc, a.ws, a.part_out);
+}
+
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
     const Partial prev = combine_ranks(a.part_in, a.world);
     publish_prev(prev, a.trace_out, a.bary_out);
-    const double M = prev.best;
-    if (!(M > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
+    if (!(prev.best > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
+    const SharedDivisor M = make_divisor(prev.best);
     const double half = a.k.half_pond;
     const double w_max = a.k.w_max;
     const uint64_t npairs = a.n >> 1;
@@ -388,11 +677,12 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     for (uint64_t k = 0; k < a.num_steps; ++k) {
         const uint64_t step = a.first_step + k;
         const bool eat = M > 0.0;
+        const SharedDivisor D = make_divisor(eat ? M : 1.0);
         Partial acc = identity();
 #pragma unroll
         for (int f = 0; f < F; ++f) {
             if (valid[f]) {
-                if (eat) w[f] = eat_weight(w[f], p[f], c[f], M, P.w_max);
+                if (eat) w[f] = eat_weight(w[f], p[f], c[f], D, P.w_max);
                 const double cn = swim(x[f], y[f], w[f], hf[f], step, P);
                 p[f] = c[f];
                 c[f] = cn;
@@ -454,11 +744,17 @@ int grid_for(uint64_t work_items, int device, int per_sm) {
 
 }  // namespace
 
-int step_grid_blocks(int device, bool explicit_cur) {
+int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
     int per_sm = 0;
-    cudaError_t e = explicit_cur
-        ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true>, kThreads, 0)
-        : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, 0);
+    cudaError_t e;
+    if (bulk && !explicit_cur) {
+        cudaFuncSetAttribute(step_kernel_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmemBytes);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_bulk, kBulkThreads, kBulkSmemBytes);
+    } else {
+        e = explicit_cur
+            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true>, kThreads, 0)
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, 0);
+    }
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     return num_sms(device) * per_sm;
 }
@@ -474,6 +770,7 @@ cudaError_t launch_init(const InitArgs& a, int grid, cudaStream_t st) {
 
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
     if (a.s.c) step_kernel<true><<<grid, kThreads, 0, st>>>(a);
+    else if (a.bulk) step_kernel_bulk<<<grid, kBulkThreads, kBulkSmemBytes, st>>>(a);
     else step_kernel<false><<<grid, kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
@@ -574,6 +871,84 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     cfg.numAttrs = 1;
     if (fpt == 1) return cudaLaunchKernelEx(&cfg, cluster_kernel<1>, a);
     return cudaLaunchKernelEx(&cfg, cluster_kernel<2>, a);
+}
+
+}  // namespace fsb_dev
+
+namespace fsb_dev {
+
+namespace {
+
+// Operand generator for the division self-test: raw 64-bit patterns (every
+// exponent, NaN, inf, subnormals, zeros) mixed with the simulation's own
+// value ranges (objective differences over a max in (0, ~sqrt(2)*pond]).
+__device__ __forceinline__ void selftest_operands(uint64_t i, uint64_t seed, double& a, double& b) {
+    const uint64_t r0 = mix64(seed ^ (2 * i + 1));
+    const uint64_t r1 = mix64(r0 + 0x9E3779B97F4A7C15ull);
+    const double u0 = unit_from_bits(r0), u1 = unit_from_bits(r1);
+    switch (i & 3) {
+        case 0:
+            a = __longlong_as_double((long long)r0);
+            b = __longlong_as_double((long long)r1);
+            break;
+        case 1:
+            a = (u0 - 0.5) * 0.4;
+            b = 1e-3 + u1 * 0.3;
+            break;
+        case 2:
+            a = (u0 - 0.5) * 300.0;
+            b = __longlong_as_double((long long)(r1 & 0x7fffffffffffffffull));
+            break;
+        default:
+            a = __longlong_as_double((long long)((r0 & 0x800fffffffffffffull) |
+                                                 ((uint64_t)(r1 % 2047) << 52)));
+            b = __longlong_as_double((long long)((r1 & 0x000fffffffffffffull) |
+                                                 ((uint64_t)((r0 >> 7) % 2047) << 52)));
+            break;
+    }
+}
+
+// Self-test of the guarded fast paths against the intrinsics.  out[0]: shared
+// divisor division, out[1]: per-operand division, out[2]: square root --
+// bitwise mismatches of (fast path, or intrinsic when the guard fails) vs the
+// intrinsic; out[3]: guard failures on simulation-range operands.
+__global__ void selftest_fast_math_kernel(uint64_t n, uint64_t seed, unsigned long long* out) {
+    unsigned long long bad[4] = {0, 0, 0, 0};
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        double a, b;
+        selftest_operands(i, seed, a, b);
+        const bool sim_range = (i & 3) == 1;
+        // division, divisor hoisted
+        double want = __ddiv_rn(a, b);
+        double q = div_shared(a, make_divisor(b));
+        if (!((q != q) && (want != want)) && __double_as_longlong(q) != __double_as_longlong(want)) ++bad[0];
+        // division, guarded per operand
+        bool ok = true;
+        q = div_guarded(a, b, ok);
+        if (!ok) q = __ddiv_rn(a, b);
+        if (sim_range && !ok) ++bad[3];
+        if (!((q != q) && (want != want)) && __double_as_longlong(q) != __double_as_longlong(want)) ++bad[1];
+        // square root (of |a| scaled into the objective's range for sim cases)
+        const double v = sim_range ? fabs(a) * 1e5 : a;
+        want = __dsqrt_rn(v);
+        ok = true;
+        q = sqrt_guarded(v, ok);
+        if (!ok) q = __dsqrt_rn(v);
+        if (sim_range && !ok && v != 0.0) ++bad[3];
+        if (!((q != q) && (want != want)) && __double_as_longlong(q) != __double_as_longlong(want)) ++bad[2];
+    }
+    for (int k = 0; k < 4; ++k)
+        if (bad[k]) atomicAdd(&out[k], bad[k]);
+}
+
+}  // namespace
+
+cudaError_t launch_selftest_fast_math(uint64_t n, uint64_t seed, unsigned long long* out, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    selftest_fast_math_kernel<<<grid_for(n, dev, 8), kThreads, 0, st>>>(n, seed, out);
+    return cudaGetLastError();
 }
 
 }  // namespace fsb_dev

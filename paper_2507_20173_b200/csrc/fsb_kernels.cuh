@@ -16,10 +16,46 @@
 
 namespace fsb_dev {
 
+// Tuning knobs (compile-time; tools/variants.py builds alternatives for A/B runs).
+#ifndef FSB_PAIRS
+#define FSB_PAIRS 1
+#endif
+#ifndef FSB_MIN_BLOCKS
+#define FSB_MIN_BLOCKS 4
+#endif
+
+// Experiment only (tools/variants.py "l2_*"): fold each CTA's memory indices
+// into its own window of FSB_MEM_WINDOW pairs so the step runs from L2 --
+// separates compute from DRAM time.  Results are meaningless with a window;
+// the product build keeps 0 (off).
+#ifndef FSB_MEM_WINDOW
+#define FSB_MEM_WINDOW 0
+#endif
+
+#ifndef FSB_BULK_STAGES
+#define FSB_BULK_STAGES 4
+#endif
+#ifndef FSB_BULK_MIN_BLOCKS
+#define FSB_BULK_MIN_BLOCKS 3
+#endif
+#ifndef FSB_BULK_PAIRS
+#define FSB_BULK_PAIRS 1
+#endif
+
 constexpr int kThreads = 256;     // threads per CTA of the streaming kernels
-constexpr int kPairsPerThread = 2;  // double2 loads per array per thread per tile
+constexpr int kPairsPerThread = FSB_PAIRS;  // double2 loads per array per thread per tile
 constexpr int kTilePairs = kThreads * kPairsPerThread;
 constexpr int kTileFish = 2 * kTilePairs;
+
+// step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,
+// plus one producer warp; a kBulkStages-deep ring of sub-tiles in smem.
+constexpr int kBulkCompute = 256;
+constexpr int kBulkThreads = kBulkCompute + 32;
+constexpr int kBulkPairsPerThread = FSB_BULK_PAIRS;
+constexpr int kBulkTilePairs = kBulkCompute * kBulkPairsPerThread;
+constexpr int kBulkStages = FSB_BULK_STAGES;
+constexpr int kBulkStageBytes = kBulkTilePairs * 16 * 4;  // x, y, w, p as double2
+constexpr int kBulkSmemBytes = kBulkStages * kBulkStageBytes;
 
 // Global partials of one step: max(prev-cur) and the barycentre sums
 // sum x*f, sum y*f, sum f.  One per rank; combined in rank order.
@@ -66,6 +102,7 @@ struct StepArgs {
     ReduceWs ws;
     Partial* part_out;    // this rank's partial of this step
     int alternate;        // reverse tile order on odd steps (L2 reuse across steps)
+    int bulk;             // stream through shared memory with cp.async.bulk (compact state)
 };
 
 struct EatArgs {
@@ -107,7 +144,7 @@ struct ClusterArgs {
     Partial* part_out;    // final step partial (for a later eat())
 };
 
-int step_grid_blocks(int device, bool explicit_cur);
+int step_grid_blocks(int device, bool explicit_cur, bool bulk);
 cudaError_t launch_init(const InitArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st);
@@ -121,5 +158,9 @@ cudaError_t launch_copy_cur(SoA s, double half_pond, uint64_t n, cudaStream_t st
 // Cluster kernel: returns cudaErrorNotSupported when n does not fit.
 int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta);
 cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st);
+
+// Self-test of the guarded fast fp64 paths vs __ddiv_rn / __dsqrt_rn on n
+// generated operands; out[4] (device) accumulates the counts (see .cu).
+cudaError_t launch_selftest_fast_math(uint64_t n, uint64_t seed, unsigned long long* out, cudaStream_t st);
 
 }  // namespace fsb_dev

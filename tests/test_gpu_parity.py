@@ -89,6 +89,20 @@ def test_sizes_bit_exact(orc, n, t, strategy, alternate):
     assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
 
 
+@pytest.mark.parametrize("n,t", [(1, 5), (513, 5), (70_001, 6), (1_000_000, 4)])
+@pytest.mark.parametrize("alternate", [True, False])
+def test_ldg_step_kernel_bit_exact(orc, n, t, alternate):
+    """The LDG (non-bulk) fused step kernel, FSB_FLAG_NO_BULK."""
+    cfg = fsb.baseline_config(n, t)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "stream", alternate=alternate, bulk=False) as eng:
+        trace, bary, _ = eng.simulate(barycentre=True)
+        got = eng.download()
+    assert got.tobytes() == want_fish.tobytes()
+    assert trace.tobytes() == want_trace.tobytes()
+    assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
+
+
 @pytest.mark.parametrize("strategy", STRATS)
 def test_per_step_barycentre(orc, strategy):
     cfg = fsb.SimConfig(num_fish=12000, pond_size=50.0, weight_scale=2.0, num_steps=12, seed=99,
@@ -287,3 +301,15 @@ def test_cpp_dropin_suite():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+def test_fast_math_selftest():
+    """The guarded fast fp64 paths of the step kernel equal __ddiv_rn / __dsqrt_rn
+    bit-for-bit on 2^27 operands (raw bit patterns incl. NaN/inf/subnormals, and
+    the simulation's ranges), and their guards never fail on in-range values."""
+    from paper_2507_20173_b200 import _native as N
+
+    out = np.zeros(4, dtype=np.uint64)
+    for seed in (1, 2):
+        N.check(N.lib().fsb_selftest_fast_math(0, 1 << 26, seed, out.ctypes.data))
+        assert out.tolist() == [0, 0, 0, 0], out

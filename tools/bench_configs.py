@@ -35,9 +35,9 @@ def peak():
         return 6650.0
 
 
-def time_cfg(name, n, t, strategy, alternate, reps):
+def time_cfg(name, n, t, strategy, alternate, reps, bulk=True):
     cfg = fsb.baseline_config(n, t)
-    with fsb.Engine(cfg, strategy=strategy, alternate=alternate) as eng:
+    with fsb.Engine(cfg, strategy=strategy, alternate=alternate, bulk=bulk) as eng:
         eng.init()
         eng.run(0, t)  # warm-up of the same shape (graph instantiation)
         secs = []
@@ -48,7 +48,7 @@ def time_cfg(name, n, t, strategy, alternate, reps):
         s = statistics.median(secs)
         ck = None
     rate = n * t / s
-    return {"config": name, "fish": n, "steps": t, "strategy": strategy, "alternate": alternate,
+    return {"config": name, "fish": n, "steps": t, "strategy": strategy, "alternate": alternate, "bulk": bulk,
             "seconds": s, "fish_updates_per_s": rate, "us_per_step": 1e6 * s / t,
             "hbm_frac_80B": rate * 80 / 1e9 / peak(), "hbm_frac_64B": rate * 64 / 1e9 / peak()}
 
@@ -58,16 +58,19 @@ def main():
     ap.add_argument("--only", default="C0,C1,C2,C3,C4")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--variants", action="store_true", help="also stream/persistent and alternate on/off")
+    ap.add_argument("--bulk-ab", action="store_true", help="also the LDG step kernel (no bulk ring)")
     a = ap.parse_args()
     for name in a.only.split(","):
         n, t = CONFIGS[name]
-        plans = [("auto", True)]
+        plans = [("auto", True, True)]
+        if a.bulk_ab and n > 32768:
+            plans += [("stream", True, False)]
         if a.variants:
-            plans += [("stream", False)]
+            plans += [("stream", False, True), ("stream", True, False)]
             if n <= 32768:
-                plans += [("stream", True), ("persistent", True)]
-        for strategy, alt in plans:
-            print(json.dumps(time_cfg(name, n, t, strategy, alt, a.reps)), flush=True)
+                plans += [("stream", True, True), ("persistent", True, True)]
+        for strategy, alt, bulk in plans:
+            print(json.dumps(time_cfg(name, n, t, strategy, alt, a.reps, bulk)), flush=True)
 
 
 if __name__ == "__main__":

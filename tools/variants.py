@@ -1,0 +1,74 @@
+#!/usr/bin/env python3
+"""A/B tuning: build compile-time variants of libfsb_b200.so and time them.
+
+    python tools/variants.py build            # here (CPU): nvcc all variants
+    python tools/variants.py run [--only C1]  # on the GPU box: bench_configs per variant
+
+Variants live in build/variants/ (git-ignored, travels to the GPU box).
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+OUT = os.path.join(ROOT, "build", "variants")
+
+VARIANTS = {
+    # LDG kernel: p<pairs per thread>b<min blocks>; bulk kernel: b<pairs>s<stages>m<min blocks>
+    "default": [],
+    "p4b2": ["-DFSB_PAIRS=4", "-DFSB_MIN_BLOCKS=2"],
+    "p1b4": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=4"],
+    "b1s4m3": ["-DFSB_BULK_PAIRS=1", "-DFSB_BULK_STAGES=4", "-DFSB_BULK_MIN_BLOCKS=3"],
+    "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
+    "b4s2m1": ["-DFSB_BULK_PAIRS=4", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=1"],
+    # experiment: LDG kernel with all memory folded into 8K pairs (compute-only time)
+    "l2_p1b4": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=4", "-DFSB_MEM_WINDOW=512"],
+    "l2_p4b2": ["-DFSB_PAIRS=4", "-DFSB_MIN_BLOCKS=2", "-DFSB_MEM_WINDOW=1024"],
+}
+
+
+def build():
+    from paper_2507_20173_b200 import _build
+
+    os.makedirs(OUT, exist_ok=True)
+    for name, flags in VARIANTS.items():
+        lib = os.path.join(OUT, f"libfsb_{name}.so")
+        cmd = [_build.nvcc(), *_build.NVCC_FLAGS, *flags, "-Xptxas", "-v", "-I", _build.INCLUDE, "-I",
+               _build.CSRC, *[os.path.join(_build.CSRC, s) for s in _build.SOURCES], "-o", lib, "-ldl"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            raise SystemExit(r.stderr)
+        regs = [l for l in r.stderr.splitlines() if "registers" in l]
+        print(name, "built;", "step regs:", [l.split("Used")[1].split(",")[0] for l in regs][:10])
+
+
+def run(only: str, reps: int, names=None):
+    for name in names or VARIANTS:
+        lib = os.path.join(OUT, f"libfsb_{name}.so")
+        env = dict(os.environ, FSB_LIB=lib)
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bench_configs.py"), "--only", only,
+                            "--reps", str(reps), "--bulk-ab"], capture_output=True, text=True, env=env)
+        for line in r.stdout.splitlines():
+            d = json.loads(line)
+            d["variant"] = name
+            print(json.dumps(d), flush=True)
+        if r.returncode:
+            print(json.dumps({"variant": name, "error": r.stderr[-500:]}), flush=True)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build()
+    else:
+        only = "C0,C1"
+        reps = 5
+        if "--only" in sys.argv:
+            only = sys.argv[sys.argv.index("--only") + 1]
+        names = None
+        if "--names" in sys.argv:
+            names = sys.argv[sys.argv.index("--names") + 1].split(",")
+        run(only, reps, names)
