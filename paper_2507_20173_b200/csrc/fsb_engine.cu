@@ -133,8 +133,9 @@ struct fsb_engine {
     uint64_t* h_step0 = nullptr;  // pinned
     double* d_scalar = nullptr;   // [4]
     int* d_mismatch = nullptr;
-    int grid = 0;
-    int grid_explicit = 0;
+    int grid = 0;            // grid of the compact-state step kernel in use
+    int grid_explicit = 0;   // grid of the explicit-cur step kernel
+    bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
 
     void* staging = nullptr;  // device AoS staging
     void* pinned = nullptr;   // host pinned staging (checksum)
@@ -222,7 +223,7 @@ fsb_dev::StepArgs step_args(fsb_engine* e, const fsb_dev::SoA& s) {
     a.ws.block_part = e->block_part;
     a.ws.counter = e->counter;
     a.alternate = (e->flags & FSB_FLAG_NO_ALTERNATE) ? 0 : 1;
-    a.bulk = (e->flags & FSB_FLAG_NO_BULK) ? 0 : 1;
+    a.bulk = e->use_bulk ? 1 : 0;
     return a;
 }
 
@@ -529,7 +530,15 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     CB(cudaMalloc(&e->s.w, bytes));
     CB(cudaMalloc(&e->s.p, bytes));
     e->s.c = nullptr;
-    e->grid = fsb_dev::step_grid_blocks(e->device, false, !(e->flags & FSB_FLAG_NO_BULK));
+    {
+        // The bulk ring pays a fill/drain per CTA: use it only when every CTA
+        // streams at least 8 sub-tiles (e.g. not for 1e6-fish L2-resident schools).
+        const int grid_bulk = fsb_dev::step_grid_blocks(e->device, false, true);
+        const uint64_t per_cta = (e->count / 2) / (uint64_t)grid_bulk;
+        e->use_bulk = !(e->flags & FSB_FLAG_NO_BULK) &&
+                      (per_cta >= 8ull * fsb_dev::kBulkTilePairs || (e->flags & FSB_FLAG_FORCE_BULK));
+        e->grid = e->use_bulk ? grid_bulk : fsb_dev::step_grid_blocks(e->device, false, false);
+    }
     e->grid_explicit = fsb_dev::step_grid_blocks(e->device, true, false);
     const int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));

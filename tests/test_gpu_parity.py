@@ -89,13 +89,15 @@ def test_sizes_bit_exact(orc, n, t, strategy, alternate):
     assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
 
 
-@pytest.mark.parametrize("n,t", [(1, 5), (513, 5), (70_001, 6), (1_000_000, 4)])
+@pytest.mark.parametrize("n,t", [(1, 5), (513, 5), (70_001, 6), (1_000_000, 4), (3_000_001, 3)])
 @pytest.mark.parametrize("alternate", [True, False])
-def test_ldg_step_kernel_bit_exact(orc, n, t, alternate):
-    """The LDG (non-bulk) fused step kernel, FSB_FLAG_NO_BULK."""
+@pytest.mark.parametrize("bulk", [False, "force"])
+def test_step_kernel_variants_bit_exact(orc, n, t, alternate, bulk):
+    """Both compact-state step kernels at every size: the LDG kernel
+    (FSB_FLAG_NO_BULK) and the cp.async.bulk ring (FSB_FLAG_FORCE_BULK)."""
     cfg = fsb.baseline_config(n, t)
     want_fish, want_trace = orc.simulate(ocfg(cfg))
-    with make(cfg, "stream", alternate=alternate, bulk=False) as eng:
+    with make(cfg, "stream", alternate=alternate, bulk=bulk) as eng:
         trace, bary, _ = eng.simulate(barycentre=True)
         got = eng.download()
     assert got.tobytes() == want_fish.tobytes()
