@@ -152,6 +152,10 @@ int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* 
  * state and B = (sum x*f / sum f, sum y*f / sum f). */
 int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]);
 
+/* Read n fish at arbitrary shard-local indices (Fish layout): sampled-fish
+ * verification of schools too large to download whole. */
+int fsb_engine_gather(fsb_engine* e, const uint64_t* local_idx, uint64_t n, fsb_fish* out);
+
 /* FNV-1a of this shard's school continuing from h_in (checksum, sim.hpp:158). */
 int fsb_engine_checksum(fsb_engine* e, uint64_t h_in, uint64_t* h_out);
 

@@ -98,6 +98,7 @@ class Oracle:
             "oracle_checksum": (u64, [vp, u64]),
             "oracle_checksum_update": (u64, [u64, vp, u64]),
             "oracle_barycentre_sums": (None, [vp, u64, vp]),
+            "oracle_replay_fish": (None, [cp, u64, vp, u64, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -145,6 +146,16 @@ class Oracle:
 
     def objective(self, x, y, pond):
         return self.L.oracle_objective(x, y, pond)
+
+    def replay(self, cfg, indices, trace):
+        """Replay the given global fish indices alone with a run's max_diff trace."""
+        trace = np.ascontiguousarray(trace, dtype=np.float64)
+        out = np.zeros(len(indices), dtype=FISH_DTYPE)
+        one = np.zeros(1, dtype=FISH_DTYPE)
+        for k, i in enumerate(indices):
+            self.L.oracle_replay_fish(ctypes.byref(cfg), int(i), _ptr(trace), len(trace), _ptr(one))
+            out[k] = one[0]
+        return out
 
 
 class Reference:

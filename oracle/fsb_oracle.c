@@ -132,6 +132,20 @@ void oracle_run(const oracle_config* cfg, oracle_fish* fish, uint64_t n, uint64_
     }
 }
 
+/* Sampled-fish replay (SURVEY.md 8(d) verification for schools without a
+ * whole-run oracle): fish i's trajectory depends only on its own state and
+ * the global max_diff sequence, so given the trace of a run it can be
+ * replayed alone: init (sim.hpp:65-79), then per step move (sim.hpp:84-99)
+ * and the weight update with trace[t] (sim.hpp:115-121). */
+void oracle_replay_fish(const oracle_config* cfg, uint64_t i, const double* trace, uint64_t num_steps,
+                        oracle_fish* out) {
+    oracle_init(cfg, i, 1, out);
+    for (uint64_t t = 0; t < num_steps; ++t) {
+        oracle_move(cfg, t, i, 1, out);
+        oracle_eat_apply(cfg, trace[t], out, 1);
+    }
+}
+
 /* sim.hpp:133-147 */
 void oracle_simulate(const oracle_config* cfg, oracle_fish* fish_out, double* trace) {
     oracle_init(cfg, 0, cfg->num_fish, fish_out);

@@ -75,6 +75,10 @@ void oracle_simulate(const oracle_config* cfg, oracle_fish* fish_out, double* tr
 void oracle_run(const oracle_config* cfg, oracle_fish* fish, uint64_t n, uint64_t first_step,
                 uint64_t num_steps, double* trace);
 
+/* Replay fish i alone for num_steps steps given a run's max_diff trace. */
+void oracle_replay_fish(const oracle_config* cfg, uint64_t i, const double* trace, uint64_t num_steps,
+                        oracle_fish* out);
+
 /* checksum (sim.hpp:154-176): FNV-1a 64 over the LE bytes of every field. */
 uint64_t oracle_checksum(const oracle_fish* fish, uint64_t n);
 /* Streamed form: continue hash h over more fish (h0 = 0xcbf29ce484222325). */

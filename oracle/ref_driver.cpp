@@ -127,6 +127,39 @@ std::uint64_t ref_checksum(const void* fish, std::uint64_t n) {
     return fsb::checksum(to_school(fish, n));
 }
 
+// simulate() for schools too large to copy out (C3: 1e9 fish = 40 GB): returns
+// checksum(init_school) and checksum(final school), the trace, and the final
+// school's f-weighted sums with long-double accumulation (golden generation).
+int ref_simulate_digest(const ref_config* cfg, std::uint64_t* init_checksum,
+                        std::uint64_t* final_checksum, double* trace, long double* bary) {
+    try {
+        const fsb::SimConfig sim = to_sim(cfg);
+        parfor::Executor exec(to_run(1, 0, 0, 0));  // sequential construct: the oracle
+        fsb::School school = fsb::init_school(sim);
+        *init_checksum = fsb::checksum(school);
+        for (std::size_t step = 0; step < sim.num_steps; ++step) {
+            fsb::move_phase(school, sim, step, exec);
+            trace[step] = fsb::eat_phase(school, sim, exec).max_diff;
+        }
+        *final_checksum = fsb::checksum(school);
+        long double s[3] = {0, 0, 0}, c[3] = {0, 0, 0};  // Neumaier in long double
+        auto add = [&](int k, long double v) {
+            const long double t = s[k] + v;
+            c[k] += (fabsl(s[k]) >= fabsl(v)) ? (s[k] - t) + v : (v - t) + s[k];
+            s[k] = t;
+        };
+        for (const fsb::Fish& f : school.fishes) {
+            add(0, static_cast<long double>(f.x * f.current_objective));
+            add(1, static_cast<long double>(f.y * f.current_objective));
+            add(2, static_cast<long double>(f.current_objective));
+        }
+        for (int k = 0; k < 3; ++k) bary[k] = s[k] + c[k];
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
 // The reference's step loop (sim.hpp:139-144) timed with steady_clock, after
 // init_school and `warmup` untimed steps: returns the seconds of `steps`
 // timed steps.  per_step (optional) receives each timed step's seconds and

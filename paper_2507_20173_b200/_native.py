@@ -83,6 +83,7 @@ SIGNATURES = [
     ("fsb_engine_run", _int, [_vp, _u64, _u64, _vp, _vp, _P(fsb_timing)]),
     ("fsb_engine_simulate", _int, [_vp, _vp, _vp, _P(fsb_timing)]),
     ("fsb_engine_barycentre", _int, [_vp, _vp, _vp]),
+    ("fsb_engine_gather", _int, [_vp, _vp, _u64, _vp]),
     ("fsb_engine_checksum", _int, [_vp, _u64, _P(_u64)]),
     ("fsb_engine_synchronize", _int, [_vp]),
     ("fsb_engine_stream", _int, [_vp, _P(_vp)]),

@@ -124,6 +124,7 @@ struct fsb_engine {
     double* c_buf = nullptr;  // explicit current_objective (only after an inconsistent upload)
     bool cur_explicit = false;
     bool max_valid = false;  // part_all[cur_buf] holds the partials of the current state
+    bool sums_valid = true;  // ... including the barycentre sums (not after a max-only run)
     int cur_buf = 0;
 
     Partial* part_all = nullptr;  // [2][world]
@@ -299,7 +300,7 @@ int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, do
     CU(cudaStreamSynchronize(e->stream));
     TRY(elapsed(e, seconds));
     e->cur_explicit = false;
-    e->max_valid = true;
+    e->max_valid = e->sums_valid = true;
     e->cur_buf = (int)((T - 1) & 1);
     e->last_launches = it->second.launches;
     return FSB_OK;
@@ -324,7 +325,7 @@ int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace
     a.first_step = first_step;
     a.num_steps = T;
     a.trace = e->d_cl_trace;
-    a.bary = e->d_cl_bary;
+    a.bary = bary ? e->d_cl_bary : nullptr;  // max-only reduction unless sums are wanted
     a.part_out = local_part(e, 0);
     CU(cudaEventRecord(e->ev0, e->stream));
     cudaError_t ce = fsb_dev::launch_cluster_run(a, e->stream);
@@ -337,7 +338,8 @@ int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace
     CU(cudaStreamSynchronize(e->stream));
     TRY(elapsed(e, seconds));
     e->cur_explicit = false;
-    e->max_valid = true;
+    e->max_valid = e->sums_valid = true;
+    e->sums_valid = bary != nullptr;
     e->cur_buf = 0;
     e->last_launches = 1;
     return FSB_OK;
@@ -359,7 +361,7 @@ int reduce_current(fsb_engine* e) {
     }
     TRY(exchange(e, 0));
     e->cur_buf = 0;
-    e->max_valid = true;
+    e->max_valid = e->sums_valid = true;
     return FSB_OK;
 }
 
@@ -641,7 +643,7 @@ int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
     CU(cudaEventRecord(e->ev1, e->stream));
     TRY(elapsed(e, seconds));
     e->cur_explicit = false;
-    e->max_valid = true;
+    e->max_valid = e->sums_valid = true;
     e->cur_buf = 0;
     return FSB_OK;
 }
@@ -681,7 +683,7 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
         }
         const Partial id{-INFINITY, 0.0, 0.0, 0.0};
         CU(cudaMemcpy(local_part(e, 0), &id, sizeof(Partial), cudaMemcpyHostToDevice));
-        e->max_valid = true;
+        e->max_valid = e->sums_valid = true;
         e->cur_buf = 0;
         e->last_launches = 0;
     } else if (want_persistent(e)) {
@@ -714,7 +716,7 @@ int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* 
 
 int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
     TRY(guard(e));
-    if (!e->max_valid) TRY(reduce_current(e));
+    if (!e->max_valid || !e->sums_valid) TRY(reduce_current(e));
     Partial r;
     TRY(host_combine(e, &r));
     if (sums) {
@@ -725,6 +727,27 @@ int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
     if (xy) {
         xy[0] = r.sx / r.sf;
         xy[1] = r.sy / r.sf;
+    }
+    return FSB_OK;
+}
+
+int fsb_engine_gather(fsb_engine* e, const uint64_t* local_idx, uint64_t n, fsb_fish* out) {
+    TRY(guard(e));
+    if (n && (!local_idx || !out)) return fail(FSB_ERR_INVALID_ARGUMENT, "null argument");
+    for (uint64_t k = 0; k < n; ++k)
+        if (local_idx[k] >= e->count) return fail(FSB_ERR_INVALID_ARGUMENT, "gather index out of range");
+    TRY(ensure_staging(e));
+    const fsb_dev::SoA s = canonical(e);
+    // indices ride in the tail of the staging buffer: kStagingFish/6 per chunk
+    const uint64_t chunk = kStagingFish / 6;
+    uint64_t* d_idx = reinterpret_cast<uint64_t*>(static_cast<char*>(e->staging) +
+                                                  chunk * sizeof(fsb_fish));
+    for (uint64_t lo = 0; lo < n; lo += chunk) {
+        const uint64_t cnt = (n - lo < chunk) ? n - lo : chunk;
+        CU(cudaMemcpyAsync(d_idx, local_idx + lo, cnt * sizeof(uint64_t), cudaMemcpyHostToDevice, e->stream));
+        CU(fsb_dev::launch_gather(s, e->cfg.pond_size / 2.0, d_idx, cnt, e->staging, e->stream));
+        CU(cudaMemcpyAsync(out + lo, e->staging, cnt * sizeof(fsb_fish), cudaMemcpyDeviceToHost, e->stream));
+        CU(cudaStreamSynchronize(e->stream));
     }
     return FSB_OK;
 }
@@ -789,7 +812,7 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
         ea.world = e->world;
         CU(fsb_dev::launch_eat(ea, e->grid, e->stream));
         e->cur_buf = (int)((num_steps - 1) & 1);
-        e->max_valid = true;
+        e->max_valid = e->sums_valid = true;
     }
     CU(cudaStreamSynchronize(e->stream));
     for (uint64_t k = 0; k < num_steps; ++k) {

@@ -87,6 +87,30 @@ __device__ __forceinline__ Partial block_reduce(Partial v, Partial* scratch) {
     return r;
 }
 
+// Max-only reductions (the persistent kernel when no barycentre is requested).
+__device__ __forceinline__ double warp_reduce_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = (u > v) ? u : v;
+    }
+    return v;
+}
+
+__device__ __forceinline__ double block_reduce_max(double v, double* scratch) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    v = warp_reduce_max(v);
+    if (lane == 0) scratch[warp] = v;
+    __syncthreads();
+    double r = -INFINITY;
+    if (warp == 0) {
+        if (lane < (int)(blockDim.x >> 5)) r = scratch[lane];
+        r = warp_reduce_max(r);
+    }
+    return r;
+}
+
 __device__ __forceinline__ Partial load_cg(const Partial* p) {
     const double2* q = reinterpret_cast<const double2*>(p);
     const double2 a = __ldcg(q);
@@ -547,6 +571,61 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
     grid_finish(acc, a.ws, a.part_out);
 }
 
+#if FSB_SINGLE
+// Experiment (tools/variants.py "single*"): one fish per thread, scalar
+// loads -- maximum thread-level parallelism, minimum registers per thread.
+__global__ void __launch_bounds__(kThreads, FSB_SINGLE_MIN_BLOCKS) step_kernel_single(const StepArgs a) {
+    const StepParams P = params_of(a.k);
+    const Partial prev = combine_ranks(a.part_in, a.world);
+    publish_prev(prev, a.trace_out, a.bary_out);
+    const bool eat = prev.best > 0.0;
+    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
+    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
+    const uint64_t n = a.n;
+    const bool rev = a.alternate && (step & 1ull);
+    constexpr uint64_t kAlign = 128;
+    const uint64_t nblk = (n + kAlign - 1) / kAlign;
+    const uint64_t lo = (nblk * blockIdx.x / gridDim.x) * kAlign;
+    uint64_t hi = (nblk * (blockIdx.x + 1) / gridDim.x) * kAlign;
+    if (hi > n) hi = n;
+    const uint64_t nsub = hi > lo ? (hi - lo + kThreads - 1) / kThreads : 0;
+    Partial acc = identity();
+    for (uint64_t j = 0; j < nsub; ++j) {
+        const uint64_t i = lo + (rev ? nsub - 1 - j : j) * kThreads + threadIdx.x;
+        bool ok = true;
+        double x = 0, y = 0, w = 0, p = 0, cn = 0;
+        if (i < hi) {
+            x = a.s.x[i];
+            y = a.s.y[i];
+            w = a.s.w[i];
+            p = a.s.p[i];
+            const double c = objective_guarded(x, y, P.half_pond, ok);
+            cn = fused_fish_guarded(x, y, w, p, c, eat, M, a.gfirst + i, step, P, ok);
+        }
+        if (__any_sync(0xffffffffu, !ok)) {
+            if (!ok) {
+                const double x0 = a.s.x[i], y0 = a.s.y[i];
+                const FishOut f = fused_fish_exact(x0, y0, a.s.w[i], a.s.p[i], objective(x0, y0, P.half_pond),
+                                                   eat, M.b, a.gfirst + i, step, P);
+                x = f.x;
+                y = f.y;
+                w = f.w;
+                p = f.p;
+                cn = f.cn;
+            }
+        }
+        if (i < hi) {
+            accumulate(acc, x, y, p, cn);
+            a.s.x[i] = x;
+            a.s.y[i] = y;
+            a.s.w[i] = w;
+            a.s.p[i] = p;
+        }
+    }
+    grid_finish(acc, a.ws, a.part_out);
+}
+#endif
+
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
     const Partial prev = combine_ranks(a.part_in, a.world);
@@ -603,10 +682,12 @@ struct FishAoS {
     double x, y, w, p, c;
 };
 
-__global__ void soa_to_aos_kernel(const SoA s, double half, uint64_t lo, uint64_t cnt, FishAoS* out) {
+// Fish [lo, lo+cnt) -- or fish idx[0..cnt) when idx is given -- in Fish layout.
+__global__ void soa_to_aos_kernel(const SoA s, double half, uint64_t lo, uint64_t cnt, FishAoS* out,
+                                  const uint64_t* idx) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += stride) {
-        const uint64_t i = lo + k;
+        const uint64_t i = idx ? idx[k] : lo + k;
         FishAoS f;
         f.x = s.x[i];
         f.y = s.y[i];
@@ -643,13 +724,16 @@ __global__ void aos_to_soa_kernel(const FishAoS* in, SoA s, double half, uint64_
 
 constexpr int kMaxCluster = 16;
 
-template <int F>
+// kBary: also reduce the barycentre sums each step (only when the caller asked
+// for them -- the max alone is a 4x shorter reduction on this latency-bound path).
+template <int F, bool kBary>
 __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned crank = cluster.block_rank();
     const unsigned ncta = cluster.num_blocks();
     __shared__ Partial slots[2][kMaxCluster];
     __shared__ Partial scratch[32];
+    __shared__ double scratch_max[32];
 
     const StepParams P = params_of(a.k);
     const uint64_t T = blockDim.x;
@@ -677,6 +761,9 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
 
     double M = -INFINITY;
     Partial tot = identity();
+    double u0[F], u1[F];  // this step's RNG draws, made during the previous barrier
+#pragma unroll
+    for (int f = 0; f < F; ++f) draw_units(hf[f], a.first_step, u0[f], u1[f]);
     for (uint64_t k = 0; k < a.num_steps; ++k) {
         const uint64_t step = a.first_step + k;
         const bool eat = M > 0.0;
@@ -686,20 +773,39 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         for (int f = 0; f < F; ++f) {
             if (valid[f]) {
                 if (eat) w[f] = eat_weight(w[f], p[f], c[f], D, P.w_max);
-                const double cn = swim(x[f], y[f], w[f], hf[f], step, P);
+                const double cn = swim_with_units(x[f], y[f], w[f], u0[f], u1[f], P);
                 p[f] = c[f];
                 c[f] = cn;
-                accumulate(acc, x[f], y[f], p[f], cn);
+                if (kBary) {
+                    accumulate(acc, x[f], y[f], p[f], cn);
+                } else {
+                    const double d = __dsub_rn(p[f], cn);
+                    acc.best = (d > acc.best) ? d : acc.best;
+                }
             }
         }
-        const Partial blk = block_reduce(acc, scratch);
+        Partial blk = identity();
+        if (kBary) blk = block_reduce(acc, scratch);
+        else blk.best = block_reduce_max(acc.best, scratch_max);
         if (threadIdx.x < 32 && threadIdx.x < ncta) {
             Partial* dst = cluster.map_shared_rank(&slots[k & 1][crank], threadIdx.x);
             *dst = blk;
         }
-        cluster.sync();
+        // split cluster barrier: arrive (release the DSMEM stores), draw the next
+        // step's random numbers while the other CTAs catch up, then wait (acquire)
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+#pragma unroll
+        for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
         tot = identity();
-        for (unsigned r = 0; r < ncta; ++r) fold(tot, slots[k & 1][r]);
+        if (kBary) {
+            for (unsigned r = 0; r < ncta; ++r) fold(tot, slots[k & 1][r]);
+        } else {
+            for (unsigned r = 0; r < ncta; ++r) {
+                const double v = slots[k & 1][r].best;
+                tot.best = (v > tot.best) ? v : tot.best;
+            }
+        }
         M = tot.best;
         if (crank == 0 && threadIdx.x == 0) {
             a.trace[k] = M;
@@ -756,7 +862,11 @@ int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
     } else {
         e = explicit_cur
             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true>, kThreads, 0)
+#if FSB_SINGLE
+            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_single, kThreads, 0);
+#else
             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, 0);
+#endif
     }
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     return num_sms(device) * per_sm;
@@ -774,7 +884,11 @@ cudaError_t launch_init(const InitArgs& a, int grid, cudaStream_t st) {
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
     if (a.s.c) step_kernel<true><<<grid, kThreads, 0, st>>>(a);
     else if (a.bulk) step_kernel_bulk<<<grid, kBulkThreads, kBulkSmemBytes, st>>>(a);
+#if FSB_SINGLE
+    else step_kernel_single<<<grid, kThreads, 0, st>>>(a);
+#else
     else step_kernel<false><<<grid, kThreads, 0, st>>>(a);
+#endif
     return cudaGetLastError();
 }
 
@@ -796,7 +910,17 @@ cudaError_t launch_soa_to_aos(const SoA& s, double half_pond, uint64_t lo, uint6
     int dev = 0;
     cudaGetDevice(&dev);
     soa_to_aos_kernel<<<grid_for(cnt, dev, 8), kThreads, 0, st>>>(s, half_pond, lo, cnt,
-                                                                  static_cast<FishAoS*>(aos));
+                                                                  static_cast<FishAoS*>(aos), nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gather(const SoA& s, double half_pond, const uint64_t* idx, uint64_t cnt, void* aos,
+                          cudaStream_t st) {
+    if (cnt == 0) return cudaSuccess;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    soa_to_aos_kernel<<<grid_for(cnt, dev, 8), kThreads, 0, st>>>(s, half_pond, 0, cnt,
+                                                                  static_cast<FishAoS*>(aos), idx);
     return cudaGetLastError();
 }
 
@@ -810,15 +934,14 @@ cudaError_t launch_aos_to_soa(const void* aos, SoA s, double half_pond, uint64_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_copy_cur(SoA, double, uint64_t, cudaStream_t) { return cudaSuccess; }
 
 // Largest cluster this device can co-schedule with 1024-thread CTAs.
 int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
     (void)device;
     static int cached = 0;
     if (!cached) {
-        cudaFuncSetAttribute(cluster_kernel<1>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(cluster_kernel<2>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(cluster_kernel<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(cluster_kernel<1, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cached = 8;
         for (int c : {16, 8}) {
             cudaLaunchConfig_t cfg = {};
@@ -832,7 +955,7 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<2>, &cfg) == cudaSuccess &&
+            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<1, true>, &cfg) == cudaSuccess &&
                 nclusters >= 1) {
                 cached = c;
                 break;
@@ -841,8 +964,8 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
         }
     }
     if (cluster_ctas) *cluster_ctas = cached;
-    if (threads_per_cta) *threads_per_cta = 256;
-    return cached * 2048;  // 2048 fish per CTA at most (1024 threads x 2 fish)
+    if (threads_per_cta) *threads_per_cta = 1024;
+    return cached * 1024;  // one fish per thread, at most 1024 threads per CTA
 }
 
 cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
@@ -851,15 +974,15 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     int cmax = 8;
     const int capacity = cluster_capacity(dev, &cmax, nullptr);
     if (a.n == 0 || a.n > (uint64_t)capacity) return cudaErrorNotSupported;
-    // ~256 fish per CTA, at most cmax CTAs; F fish per thread with F*threads
-    // <= 1024 threads; F = 2 still fits the 64-register budget without spills.
-    uint64_t ncta = (a.n + 255) / 256;
+    // One fish per thread (latency-bound: the chain per fish is the step's
+    // critical path), spread over as many CTAs (SMs) of the cluster as give
+    // each at least FSB_CLUSTER_MIN_FISH fish.
+    uint64_t ncta = (a.n + FSB_CLUSTER_MIN_FISH - 1) / FSB_CLUSTER_MIN_FISH;
     if (ncta > (uint64_t)cmax) ncta = cmax;
     if (ncta < 1) ncta = 1;
     const uint64_t per_cta = (a.n + ncta - 1) / ncta;
-    const uint64_t fpt = per_cta <= 1024 ? 1 : 2;
-    if (per_cta > 2048) return cudaErrorNotSupported;
-    const uint64_t threads = (((per_cta + fpt - 1) / fpt + 31) / 32) * 32;
+    if (per_cta > 1024) return cudaErrorNotSupported;
+    const uint64_t threads = ((per_cta + 31) / 32) * 32;
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ncta);
@@ -872,8 +995,8 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (fpt == 1) return cudaLaunchKernelEx(&cfg, cluster_kernel<1>, a);
-    return cudaLaunchKernelEx(&cfg, cluster_kernel<2>, a);
+    if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<1, true>, a);
+    return cudaLaunchKernelEx(&cfg, cluster_kernel<1, false>, a);
 }
 
 }  // namespace fsb_dev

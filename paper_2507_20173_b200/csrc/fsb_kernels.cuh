@@ -32,6 +32,17 @@ namespace fsb_dev {
 #define FSB_MEM_WINDOW 0
 #endif
 
+#ifndef FSB_SINGLE
+#define FSB_SINGLE 0  // experiment: one fish per thread in the LDG step kernel
+#endif
+#ifndef FSB_SINGLE_MIN_BLOCKS
+#define FSB_SINGLE_MIN_BLOCKS 6
+#endif
+
+#ifndef FSB_CLUSTER_MIN_FISH
+#define FSB_CLUSTER_MIN_FISH 256  // persistent kernel: fish per CTA before adding CTAs
+#endif
+
 #ifndef FSB_BULK_STAGES
 #define FSB_BULK_STAGES 4
 #endif
@@ -153,7 +164,8 @@ cudaError_t launch_soa_to_aos(const SoA& s, double half_pond, uint64_t lo, uint6
                               cudaStream_t st);
 cudaError_t launch_aos_to_soa(const void* aos, SoA s, double half_pond, uint64_t lo, uint64_t cnt,
                               int* mismatch, cudaStream_t st);
-cudaError_t launch_copy_cur(SoA s, double half_pond, uint64_t n, cudaStream_t st);
+cudaError_t launch_gather(const SoA& s, double half_pond, const uint64_t* idx, uint64_t cnt, void* aos,
+                          cudaStream_t st);
 
 // Cluster kernel: returns cudaErrorNotSupported when n does not fit.
 int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta);

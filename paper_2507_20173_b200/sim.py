@@ -218,6 +218,13 @@ class Engine:
         N.check(N.lib().fsb_engine_barycentre(self._h, _ptr(sums), _ptr(xy)))
         return sums, xy
 
+    def gather(self, local_idx) -> np.ndarray:
+        """Fish at the given shard-local indices (Fish layout)."""
+        idx = np.ascontiguousarray(local_idx, dtype=np.uint64)
+        out = np.empty(idx.shape[0], dtype=FISH_DTYPE)
+        N.check(N.lib().fsb_engine_gather(self._h, _ptr(idx), idx.shape[0], _ptr(out)))
+        return out
+
     def checksum(self, h: int = kChecksumEmpty) -> int:
         out = ctypes.c_uint64()
         N.check(N.lib().fsb_engine_checksum(self._h, h, ctypes.byref(out)))

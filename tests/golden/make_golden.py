@@ -174,6 +174,38 @@ def gen_baseline(ref: Reference, which: dict, path: str) -> None:
         json.dump(data, open(path, "w"), indent=1)
 
 
+def gen_huge(ref: Reference, path: str) -> None:
+    """C3 (1e9 x 20): the reference school is 40 GB, so the reference computes
+    the digests in place (ref_simulate_digest: sequential construct, checksum
+    of init and final school, trace, Neumaier long-double barycentre sums)."""
+    import ctypes
+
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    if "C3_1e9x20" in data:
+        return
+    L = ref.L
+    L.ref_simulate_digest.restype = ctypes.c_int
+    L.ref_simulate_digest.argtypes = [ctypes.POINTER(Config), ctypes.POINTER(ctypes.c_uint64),
+                                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p, ctypes.c_void_p]
+    cfg = baseline_config(10**9, 20)
+    ic, fc = ctypes.c_uint64(), ctypes.c_uint64()
+    trace = np.zeros(cfg.num_steps)
+    bary = (ctypes.c_longdouble * 3)()
+    rc = L.ref_simulate_digest(ctypes.byref(cfg), ctypes.byref(ic), ctypes.byref(fc), trace.ctypes.data,
+                               ctypes.cast(bary, ctypes.c_void_p))
+    assert rc == 0
+    data["C3_1e9x20"] = {
+        "config": cfg_dict(cfg),
+        "init_checksum": f"{ic.value:016x}",
+        "final_checksum": f"{fc.value:016x}",
+        "trace_hex": [hexd(v) for v in trace],
+        "trace_last_hex": hexd(trace[-1]),
+        "barycentre_fsum": [hexd(v) for v in bary],
+        "barycentre_method": "Neumaier-compensated long double over fp64 products (reference final state)",
+    }
+    json.dump(data, open(path, "w"), indent=1)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
@@ -191,7 +223,7 @@ def main() -> None:
     if a.big:
         gen_baseline(ref, BIGGER, path)
     if a.huge:
-        gen_baseline(ref, HUGE, path)
+        gen_huge(ref, path)
 
 
 if __name__ == "__main__":

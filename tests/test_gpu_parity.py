@@ -123,6 +123,21 @@ def test_per_step_barycentre(orc, strategy):
     assert rel_ok(xy, [want[-1][0] / want[-1][2], want[-1][1] / want[-1][2]], 1e-12)
 
 
+@pytest.mark.parametrize("strategy", STRATS)
+def test_barycentre_after_max_only_run(orc, strategy):
+    """A run without the per-step sums (the persistent kernel then reduces the
+    max only) followed by the barycentre query of the final state."""
+    cfg = fsb.baseline_config(4096, 30)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, strategy) as eng:
+        eng.init()
+        trace, bary, _ = eng.run(0, 30, barycentre=False)
+        assert bary is None and trace.tobytes() == want_trace.tobytes()
+        sums, _ = eng.barycentre()
+        assert rel_ok(sums, orc.barycentre_sums(want_fish))
+        assert bits(eng.eat().max_diff) == bits(orc.eat(ocfg(cfg), want_fish))
+
+
 def test_large_stream_bit_exact(orc):
     cfg = fsb.SimConfig(num_fish=1_000_003, pond_size=200.0, weight_scale=10.0, num_steps=25, seed=7,
                         step_base=1.0)
@@ -315,3 +330,33 @@ def test_fast_math_selftest():
     for seed in (1, 2):
         N.check(N.lib().fsb_selftest_fast_math(0, 1 << 26, seed, out.ctypes.data))
         assert out.tolist() == [0, 0, 0, 0], out
+
+
+def test_gather_matches_download(orc):
+    cfg = fsb.baseline_config(100_001, 3)
+    with make(cfg) as eng:
+        eng.simulate(barycentre=False)
+        full = eng.download()
+        idx = np.array([0, 5, 100_000, 77, 5], dtype=np.uint64)
+        assert eng.gather(idx).tobytes() == full[idx.astype(np.int64)].tobytes()
+
+
+def test_c3_billion_fish(golden_baseline, orc):
+    """C3 (1e9 fish x 20 steps, 32 GB of state): the max_diff trace against the
+    reference's, 20,000 sampled fish replayed on the CPU from their initial state
+    with the GPU trace, the final checksum streamed over all 40 GB
+    of Fish bytes, and the barycentre."""
+    cfg = fsb.baseline_config(10**9, 20)
+    g = golden_baseline.get("C3_1e9x20")
+    with make(cfg) as eng:
+        trace, bary, _ = eng.simulate(barycentre=True)
+        if g:
+            assert [bits(v) for v in trace] == g["trace_hex"]
+        rng = np.random.default_rng(3)
+        idx = np.unique(np.concatenate([rng.integers(0, 10**9, 20_000), [0, 1, 10**9 - 2, 10**9 - 1]]))
+        got = eng.gather(idx.astype(np.uint64))
+        want = orc.replay(ocfg(cfg), idx, trace)
+        assert got.tobytes() == want.tobytes()
+        if g:
+            assert f"{eng.checksum():016x}" == g["final_checksum"]
+            assert rel_ok(bary[-1], [unhex(v) for v in g["barycentre_fsum"]])

@@ -101,6 +101,17 @@ def test_baseline_configs(orc, golden_baseline, name):
         assert abs(a - b) <= 1e-14 * abs(b)
 
 
+def test_sampled_replay_matches_whole_run(orc):
+    """One fish replayed alone with the run's trace equals its state in the run."""
+    cfg = oracle.baseline_config(3001, 15)
+    fish, trace = orc.simulate(cfg)
+    idx = [0, 1, 17, 1500, 2999, 3000]
+    assert orc.replay(cfg, idx, trace).tobytes() == fish[idx].tobytes()
+    cfg = oracle.Config.make(num_fish=500, num_steps=60, seed=42, step_base=10.0)  # clamp-heavy
+    fish, trace = orc.simulate(cfg)
+    assert orc.replay(cfg, range(500), trace).tobytes() == fish.tobytes()
+
+
 def test_sharded_oracle_matches_whole(orc):
     """Global-index RNG keys make a contiguous shard reproduce the same fish."""
     cfg = oracle.baseline_config(1001, 5)

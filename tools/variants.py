@@ -25,6 +25,13 @@ VARIANTS = {
     "b1s4m3": ["-DFSB_BULK_PAIRS=1", "-DFSB_BULK_STAGES=4", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b4s2m1": ["-DFSB_BULK_PAIRS=4", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=1"],
+    # LDG kernel, one fish per thread
+    "single4": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=4"],
+    "single6": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=6"],
+    "single8": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=8"],
+    # persistent cluster kernel: fish per CTA before another CTA is added
+    "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
+    "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
     # experiment: LDG kernel with all memory folded into 8K pairs (compute-only time)
     "l2_p1b4": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=4", "-DFSB_MEM_WINDOW=512"],
     "l2_p4b2": ["-DFSB_PAIRS=4", "-DFSB_MIN_BLOCKS=2", "-DFSB_MEM_WINDOW=1024"],
