@@ -12,6 +12,7 @@
 #include <exception>
 #include <stdexcept>
 
+#include "fsb/csv.hpp"
 #include "fsb/sim.hpp"
 
 namespace {
@@ -125,6 +126,23 @@ int ref_simulate(const ref_config* cfg, int threads, int sched_kind, std::uint64
 
 std::uint64_t ref_checksum(const void* fish, std::uint64_t n) {
     return fsb::checksum(to_school(fish, n));
+}
+
+// The reference's own CSV reader (csv.hpp:114-145) and validator (:161-179)
+// applied to a results text: returns the record count (or -1 on a CsvError,
+// message in err) and the number of validate_records diagnostics in *issues.
+int ref_read_csv(const char* text, int* issues, char* err, int errlen) {
+    try {
+        const std::vector<fsb::BenchRecord> recs = fsb::read_csv_string(text);
+        if (issues) *issues = static_cast<int>(fsb::validate_records(recs).size());
+        return static_cast<int>(recs.size());
+    } catch (const std::exception& e) {
+        if (err && errlen > 0) {
+            std::strncpy(err, e.what(), static_cast<std::size_t>(errlen - 1));
+            err[errlen - 1] = 0;
+        }
+        return -1;
+    }
 }
 
 // simulate() for schools too large to copy out (C3: 1e9 fish = 40 GB): returns

@@ -332,6 +332,24 @@ def test_fast_math_selftest():
         assert out.tolist() == [0, 0, 0, 0], out
 
 
+def test_cli_simulate_record(tmp_path, capsys):
+    """`simulate` with the reference CLI's flags (cli.hpp:179-207): the record's
+    checksum is the reference digest of SimConfig{fish 1e4, steps 100, seed 7}
+    (acceptance.cpp:63-102 / SURVEY App. C) and the row is in the reference schema."""
+    from paper_2507_20173_b200 import records
+    from paper_2507_20173_b200.__main__ import main as cli_main
+
+    out = tmp_path / "r.csv"
+    assert cli_main(["simulate", "--fish", "10000", "--steps", "100", "--seed", "7", "--out", str(out)]) == 0
+    recs = records.read_csv(out.read_text())
+    assert len(recs) == 1 and recs[0].checksum == 0xF7E6675CBE28EB38
+    assert recs[0].construct == "gpu" and recs[0].seconds_eat <= recs[0].seconds_total
+    assert cli_main(["gpuexp", "--fish", "4096", "--steps", "50", "--reps", "2", "--warmup", "1",
+                     "--out", str(out)]) == 0
+    recs = records.read_csv(out.read_text())
+    assert len(recs) == 6 and len({r.checksum for r in recs}) == 1 and not any(r.failed() for r in recs)
+
+
 def test_gather_matches_download(orc):
     cfg = fsb.baseline_config(100_001, 3)
     with make(cfg) as eng:
