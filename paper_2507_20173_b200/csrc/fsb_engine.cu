@@ -560,6 +560,12 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
         std::memcpy(&id, o.nccl_unique_id, sizeof id);
         ncclResult_t r = g_nccl.CommInitRank(&e->comm, e->world, id, e->rank);
         if (r != ncclSuccess) return bail(nccl_fail(r, "ncclCommInitRank"));
+        // One eager exchange so NCCL sets up its (lazily established) connections
+        // outside any CUDA-graph capture.
+        CB(cudaMemsetAsync(e->part_all, 0, 2 * e->world * sizeof(Partial), e->stream));
+        rc = exchange(e, 0);
+        if (rc != FSB_OK) return bail(rc);
+        CB(cudaStreamSynchronize(e->stream));
     }
 #undef CB
     *out = e;

@@ -719,10 +719,42 @@ __global__ void aos_to_soa_kernel(const FishAoS* in, SoA s, double half, uint64_
 
 // ---------------------------------------------------------------------------
 // Small-swarm persistent kernel: one cluster of C CTAs holds the whole school
-// in registers for every step; the per-step global max + sums go through
-// distributed shared memory and one cluster barrier per step.
+// in registers for every step.  The per-step exchange has no cluster barrier:
+// each CTA pushes its partial into every CTA's slot with st.async, whose bytes
+// complete a transaction count on the DESTINATION CTA's mbarrier; each CTA then
+// waits on its own mbarrier until all C partials have landed.  Double-buffered
+// by step parity; a CTA can reuse a slot only after every CTA has consumed it
+// (it needs their next partials first), so no further synchronisation is needed.
 
 constexpr int kMaxCluster = 16;
+
+__device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem, unsigned rank) {
+    uint32_t r;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void st_async_f64x2(uint32_t dst, double a, double b, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
+                 "d"(a), "d"(b), "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void st_async_f64(uint32_t dst, double a, uint32_t bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(dst), "d"(a),
+                 "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "FSB_CWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra FSB_CWAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 
 // kBary: also reduce the barycentre sums each step (only when the caller asked
 // for them -- the max alone is a 4x shorter reduction on this latency-bound path).
@@ -731,9 +763,17 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned crank = cluster.block_rank();
     const unsigned ncta = cluster.num_blocks();
-    __shared__ Partial slots[2][kMaxCluster];
+    __shared__ __align__(16) Partial slots[2][kMaxCluster];
+    __shared__ __align__(8) uint64_t xbar[2];
     __shared__ Partial scratch[32];
     __shared__ double scratch_max[32];
+    constexpr unsigned kBytes = kBary ? 32 : 8;  // bytes each CTA pushes per destination
+    if (threadIdx.x == 0) {
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();  // every CTA's barriers exist before anyone pushes into them
 
     const StepParams P = params_of(a.k);
     const uint64_t T = blockDim.x;
@@ -766,6 +806,8 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     for (int f = 0; f < F; ++f) draw_units(hf[f], a.first_step, u0[f], u1[f]);
     for (uint64_t k = 0; k < a.num_steps; ++k) {
         const uint64_t step = a.first_step + k;
+        const unsigned b = (unsigned)(k & 1);
+        if (threadIdx.x == 0) mbar_expect_tx(&xbar[b], ncta * kBytes);  // may race the pushes: fine
         const bool eat = M > 0.0;
         const SharedDivisor D = make_divisor(eat ? M : 1.0);
         Partial acc = identity();
@@ -787,16 +829,20 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         Partial blk = identity();
         if (kBary) blk = block_reduce(acc, scratch);
         else blk.best = block_reduce_max(acc.best, scratch_max);
-        if (threadIdx.x < 32 && threadIdx.x < ncta) {
-            Partial* dst = cluster.map_shared_rank(&slots[k & 1][crank], threadIdx.x);
-            *dst = blk;
+        if (threadIdx.x < 32 && threadIdx.x < ncta) {  // lane r pushes this CTA's partial to CTA r
+            const uint32_t dst = cluster_map(smem_u32(&slots[b][crank]), threadIdx.x);
+            const uint32_t bar = cluster_map(smem_u32(&xbar[b]), threadIdx.x);
+            if (kBary) {
+                st_async_f64x2(dst, blk.best, blk.sx, bar);
+                st_async_f64x2(dst + 16, blk.sy, blk.sf, bar);
+            } else {
+                st_async_f64(dst, blk.best, bar);
+            }
         }
-        // split cluster barrier: arrive (release the DSMEM stores), draw the next
-        // step's random numbers while the other CTAs catch up, then wait (acquire)
-        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+        // draw the next step's random numbers while the partials travel
 #pragma unroll
         for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
-        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        mbar_wait_cluster(&xbar[b], (unsigned)((k >> 1) & 1));
         tot = identity();
         if (kBary) {
             for (unsigned r = 0; r < ncta; ++r) fold(tot, slots[k & 1][r]);
@@ -830,6 +876,7 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         }
     }
     if (a.num_steps > 0 && crank == 0 && threadIdx.x == 0) store_partial(a.part_out, tot);
+    cluster.sync();  // no CTA retires while a peer could still address its shared memory
 }
 
 int g_num_sms[64] = {0};
