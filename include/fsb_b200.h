@@ -78,6 +78,7 @@ enum fsb_strategy {
 #define FSB_FLAG_FORCE_NCCL 0x2u   /* use the NCCL exchange even when world_size == 1 (testing) */
 #define FSB_FLAG_NO_BULK 0x4u      /* step kernel loads with LDG instead of the cp.async.bulk smem ring */
 #define FSB_FLAG_FORCE_BULK 0x8u   /* bulk ring even for schools too small to amortise it (testing) */
+#define FSB_FLAG_NO_PDL 0x10u      /* no Programmatic Dependent Launch between graph step kernels */
 
 typedef struct fsb_engine_options {
     int device;                  /* CUDA device ordinal of this shard */

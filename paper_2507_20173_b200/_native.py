@@ -27,6 +27,7 @@ FLAG_NO_ALTERNATE = 0x1
 FLAG_FORCE_NCCL = 0x2
 FLAG_NO_BULK = 0x4
 FLAG_FORCE_BULK = 0x8
+FLAG_NO_PDL = 0x10
 
 
 class fsb_sim_config(ctypes.Structure):

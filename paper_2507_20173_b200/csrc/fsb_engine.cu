@@ -233,6 +233,10 @@ fsb_dev::StepArgs step_args(fsb_engine* e, const fsb_dev::SoA& s) {
 // eat kernel applies step T-1's eat.  The first step index is read at run time
 // from d_step0 (filled by the graph's first node from pinned memory), so one
 // graph serves every first_step.
+// Programmatic Dependent Launch between consecutive step kernels of a graph:
+// not across an NCCL exchange (its kernel does not release dependents early).
+bool use_pdl(const fsb_engine* e) { return !e->use_nccl && !(e->flags & FSB_FLAG_NO_PDL); }
+
 int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out) {
     GraphEntry g;
     CU(cudaMalloc(&g.d_trace, T * sizeof(double)));
@@ -252,6 +256,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         a.trace_out = k ? g.d_trace + (k - 1) : nullptr;
         a.bary_out = k ? g.d_bary + 3 * (k - 1) : nullptr;
         a.part_out = local_part(e, (int)(k & 1));
+        a.pdl = (k > 0 && use_pdl(e)) ? 1 : 0;  // kernel -> kernel edges only
         ce = fsb_dev::launch_step(a, (k == 0 && explicit_first) ? e->grid_explicit : e->grid, e->stream);
         ++launches;
         if (ce == cudaSuccess) rc = exchange(e, (int)(k & 1));
@@ -266,6 +271,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         ea.world = e->world;
         ea.trace_out = g.d_trace + (T - 1);
         ea.bary_out = g.d_bary + 3 * (T - 1);
+        ea.pdl = use_pdl(e) ? 1 : 0;
         ce = fsb_dev::launch_eat(ea, e->grid, e->stream);
         ++launches;
     }

@@ -154,6 +154,14 @@ __device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs
     }
 }
 
+// Programmatic Dependent Launch: block until the predecessor grid has completed
+// and flushed (no-op when not launched as a dependent), then let the next
+// kernel in the stream be scheduled as our CTAs retire.
+__device__ __forceinline__ void pdl_wait_and_release() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Combine the ranks' partials of the previous step in rank order.
 __device__ __forceinline__ Partial combine_ranks(const Partial* part_in, int world) {
     Partial r = identity();
@@ -306,6 +314,7 @@ __global__ void __launch_bounds__(kThreads) init_kernel(const InitArgs a) {
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
     const StepParams P = params_of(a.k);
+    pdl_wait_and_release();
     const Partial prev = combine_ranks(a.part_in, a.world);
     publish_prev(prev, a.trace_out, a.bary_out);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
@@ -451,6 +460,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
     __shared__ __align__(8) uint64_t empty[kBulkStages];
 
     const StepParams P = params_of(a.k);
+    pdl_wait_and_release();
     const Partial prev = combine_ranks(a.part_in, a.world);
     publish_prev(prev, a.trace_out, a.bary_out);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
@@ -576,6 +586,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
 // loads -- maximum thread-level parallelism, minimum registers per thread.
 __global__ void __launch_bounds__(kThreads, FSB_SINGLE_MIN_BLOCKS) step_kernel_single(const StepArgs a) {
     const StepParams P = params_of(a.k);
+    pdl_wait_and_release();
     const Partial prev = combine_ranks(a.part_in, a.world);
     publish_prev(prev, a.trace_out, a.bary_out);
     const bool eat = prev.best > 0.0;
@@ -628,6 +639,7 @@ __global__ void __launch_bounds__(kThreads, FSB_SINGLE_MIN_BLOCKS) step_kernel_s
 
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
+    pdl_wait_and_release();
     const Partial prev = combine_ranks(a.part_in, a.world);
     publish_prev(prev, a.trace_out, a.bary_out);
     if (!(prev.best > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
@@ -928,21 +940,40 @@ cudaError_t launch_init(const InitArgs& a, int grid, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// Launch with Programmatic Dependent Launch when requested: the kernel may be
+// scheduled while its predecessor drains; it waits in griddepcontrol.wait
+// (pdl_wait) before touching anything the predecessor wrote.
+template <typename Args>
+cudaError_t launch_maybe_pdl(void (*kern)(Args), int grid, int block, size_t smem, cudaStream_t st,
+                             const Args& a, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
-    if (a.s.c) step_kernel<true><<<grid, kThreads, 0, st>>>(a);
-    else if (a.bulk) step_kernel_bulk<<<grid, kBulkThreads, kBulkSmemBytes, st>>>(a);
+    const bool pdl = a.pdl != 0;
+    if (a.s.c) return launch_maybe_pdl(step_kernel<true>, grid, kThreads, 0, st, a, pdl);
+    if (a.bulk) return launch_maybe_pdl(step_kernel_bulk, grid, kBulkThreads, kBulkSmemBytes, st, a, pdl);
 #if FSB_SINGLE
-    else step_kernel_single<<<grid, kThreads, 0, st>>>(a);
+    return launch_maybe_pdl(step_kernel_single, grid, kThreads, 0, st, a, pdl);
 #else
-    else step_kernel<false><<<grid, kThreads, 0, st>>>(a);
+    return launch_maybe_pdl(step_kernel<false>, grid, kThreads, 0, st, a, pdl);
 #endif
-    return cudaGetLastError();
 }
 
 cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st) {
-    if (a.s.c) eat_kernel<true><<<grid, kThreads, 0, st>>>(a);
-    else eat_kernel<false><<<grid, kThreads, 0, st>>>(a);
-    return cudaGetLastError();
+    const bool pdl = a.pdl != 0;
+    if (a.s.c) return launch_maybe_pdl(eat_kernel<true>, grid, kThreads, 0, st, a, pdl);
+    return launch_maybe_pdl(eat_kernel<false>, grid, kThreads, 0, st, a, pdl);
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, int grid, cudaStream_t st) {

@@ -114,6 +114,7 @@ struct StepArgs {
     Partial* part_out;    // this rank's partial of this step
     int alternate;        // reverse tile order on odd steps (L2 reuse across steps)
     int bulk;             // stream through shared memory with cp.async.bulk (compact state)
+    int pdl;              // launched as a programmatic dependent of the previous step
 };
 
 struct EatArgs {
@@ -124,6 +125,7 @@ struct EatArgs {
     int world;
     double* trace_out;
     double* bary_out;
+    int pdl;
 };
 
 struct ReduceArgs {

@@ -35,9 +35,9 @@ def peak():
         return 6650.0
 
 
-def time_cfg(name, n, t, strategy, alternate, reps, bulk=True):
+def time_cfg(name, n, t, strategy, alternate, reps, bulk=True, pdl=True):
     cfg = fsb.baseline_config(n, t)
-    with fsb.Engine(cfg, strategy=strategy, alternate=alternate, bulk=bulk) as eng:
+    with fsb.Engine(cfg, strategy=strategy, alternate=alternate, bulk=bulk, pdl=pdl) as eng:
         eng.init()
         eng.run(0, t)  # warm-up of the same shape (graph instantiation)
         secs = []
@@ -49,6 +49,7 @@ def time_cfg(name, n, t, strategy, alternate, reps, bulk=True):
         ck = None
     rate = n * t / s
     return {"config": name, "fish": n, "steps": t, "strategy": strategy, "alternate": alternate, "bulk": bulk,
+            "pdl": pdl,
             "seconds": s, "fish_updates_per_s": rate, "us_per_step": 1e6 * s / t,
             "hbm_frac_80B": rate * 80 / 1e9 / peak(), "hbm_frac_64B": rate * 64 / 1e9 / peak()}
 
@@ -59,6 +60,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--variants", action="store_true", help="also stream/persistent and alternate on/off")
     ap.add_argument("--bulk-ab", action="store_true", help="also the LDG step kernel (no bulk ring)")
+    ap.add_argument("--pdl-ab", action="store_true", help="also without programmatic dependent launch")
     a = ap.parse_args()
     for name in a.only.split(","):
         n, t = CONFIGS[name]
@@ -71,6 +73,8 @@ def main():
                 plans += [("stream", True, True), ("persistent", True, True)]
         for strategy, alt, bulk in plans:
             print(json.dumps(time_cfg(name, n, t, strategy, alt, a.reps, bulk)), flush=True)
+        if a.pdl_ab and n > 32768:
+            print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, True, pdl=False)), flush=True)
 
 
 if __name__ == "__main__":
