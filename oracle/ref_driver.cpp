@@ -128,6 +128,25 @@ std::uint64_t ref_checksum(const void* fish, std::uint64_t n) {
     return fsb::checksum(to_school(fish, n));
 }
 
+// The reference step loop (sequential construct) with checksum(school) taken
+// after every `every`-th step in place: digests[k] after step (k+1)*every - 1.
+int ref_step_digests(const ref_config* cfg, std::uint64_t every, std::uint64_t* digests, double* trace) {
+    try {
+        const fsb::SimConfig sim = to_sim(cfg);
+        parfor::Executor exec(to_run(1, 0, 0, 0));
+        fsb::School school = fsb::init_school(sim);
+        for (std::size_t step = 0; step < sim.num_steps; ++step) {
+            fsb::move_phase(school, sim, step, exec);
+            const double m = fsb::eat_phase(school, sim, exec).max_diff;
+            if (trace) trace[step] = m;
+            if ((step + 1) % every == 0) digests[(step + 1) / every - 1] = fsb::checksum(school);
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
 // The reference's own CSV reader (csv.hpp:114-145) and validator (:161-179)
 // applied to a results text: returns the record count (or -1 on a CsvError,
 // message in err) and the number of validate_records diagnostics in *issues.

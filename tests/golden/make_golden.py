@@ -174,6 +174,28 @@ def gen_baseline(ref: Reference, which: dict, path: str) -> None:
         json.dump(data, open(path, "w"), indent=1)
 
 
+def gen_step_digests(ref: Reference, path: str) -> None:
+    """SURVEY 8(d) gates: the reference checksum after EVERY step for C0 and C1,
+    and after every 1000th step for C4 (ref_step_digests, in place)."""
+    import ctypes
+
+    data = json.load(open(path)) if os.path.exists(path) else {}
+    L = ref.L
+    L.ref_step_digests.restype = ctypes.c_int
+    L.ref_step_digests.argtypes = [ctypes.POINTER(Config), ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+    for name, every in (("C0_1e6x100", 1), ("C1_1e7x100", 1), ("C4_4096x100000", 1000)):
+        if name not in data or "step_checksums" in data[name]:
+            continue
+        cfg = Config.make(**data[name]["config"])
+        digests = np.zeros(cfg.num_steps // every, dtype=np.uint64)
+        assert L.ref_step_digests(ctypes.byref(cfg), every, digests.ctypes.data, None) == 0
+        data[name]["step_checksums"] = [f"{int(d):016x}" for d in digests]
+        data[name]["step_checksums_every"] = every
+        assert data[name]["step_checksums"][-1] == data[name]["final_checksum"]
+        print(f"  {name}: {len(digests)} per-step digests", flush=True)
+        json.dump(data, open(path, "w"), indent=1)
+
+
 def gen_huge(ref: Reference, path: str) -> None:
     """C3 (1e9 x 20): the reference school is 40 GB, so the reference computes
     the digests in place (ref_simulate_digest: sequential construct, checksum
@@ -220,6 +242,7 @@ def main() -> None:
     print("baseline configs", flush=True)
     path = os.path.join(HERE, "baseline_digests.json")
     gen_baseline(ref, BIG, path)
+    gen_step_digests(ref, path)
     if a.big:
         gen_baseline(ref, BIGGER, path)
     if a.huge:

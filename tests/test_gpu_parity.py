@@ -310,6 +310,21 @@ def test_baseline_configs_match_reference_digests(golden_baseline, orc, name):
     assert rel_ok(bary[-1], [unhex(v) for v in g["barycentre_fsum"]])
 
 
+@pytest.mark.parametrize("name", ["C0_1e6x100", "C1_1e7x100", "C4_4096x100000"])
+def test_baseline_configs_every_step(golden_baseline, name):
+    """SURVEY 8(d) correctness gates: the reference checksum after every step
+    (C0, C1) or every 1000th step (C4), the engine run chunk by chunk."""
+    g = golden_baseline[name]
+    every = g["step_checksums_every"]
+    cfg = fsb.SimConfig(**g["config"])
+    with make(cfg) as eng:
+        eng.init()
+        assert f"{eng.checksum():016x}" == g["init_checksum"]
+        for k, want in enumerate(g["step_checksums"]):
+            eng.run(k * every, every)
+            assert f"{eng.checksum():016x}" == want, f"after step {(k + 1) * every - 1}"
+
+
 def test_cpp_dropin_suite():
     """tests/cpp/test_gpu_sim: the reference's test_sim.cpp cases via fsb::gpu."""
     exe = os.path.join(ROOT, "tests", "cpp", "test_gpu_sim")
