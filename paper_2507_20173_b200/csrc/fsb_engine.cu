@@ -293,6 +293,7 @@ int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, do
     const auto key = std::make_pair(T, e->cur_explicit ? 1 : 0);
     auto it = e->graphs.find(key);
     if (it == e->graphs.end()) {
+        if (e->graphs.size() >= 16) free_graphs(e);  // bound the cache (distinct step counts)
         GraphEntry g;
         TRY(build_graph(e, T, e->cur_explicit, &g));
         it = e->graphs.emplace(key, g).first;
@@ -681,6 +682,26 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     return FSB_OK;
 }
 
+// Long runs are cut into graphs of at most kMaxGraphSteps steps (each a
+// complete run: its own trailing eat), so graph size stays bounded.
+int run_stream_chunked(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
+                       double* seconds) {
+    constexpr uint64_t kMaxGraphSteps = 1024;
+    double total = 0.0;
+    uint64_t launches = 0;
+    for (uint64_t off = 0; off < T; off += kMaxGraphSteps) {
+        const uint64_t len = (T - off < kMaxGraphSteps) ? T - off : kMaxGraphSteps;
+        double s = 0.0;
+        TRY(run_stream(e, first_step + off, len, trace ? trace + off : nullptr, bary ? bary + 3 * off : nullptr,
+                       &s));
+        total += s;
+        launches += e->last_launches;
+    }
+    *seconds = total;
+    e->last_launches = launches;
+    return FSB_OK;
+}
+
 int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* trace, double* bary,
                    fsb_timing* timing) {
     TRY(guard(e));
@@ -701,10 +722,10 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
     } else if (want_persistent(e)) {
         int rc = run_persistent(e, first_step, num_steps, trace, bary, &secs);
         if (rc == FSB_ERR_UNSUPPORTED && e->strategy == FSB_STRATEGY_AUTO)
-            rc = run_stream(e, first_step, num_steps, trace, bary, &secs);
+            rc = run_stream_chunked(e, first_step, num_steps, trace, bary, &secs);
         TRY(rc);
     } else {
-        TRY(run_stream(e, first_step, num_steps, trace, bary, &secs));
+        TRY(run_stream_chunked(e, first_step, num_steps, trace, bary, &secs));
     }
     if (timing) {
         timing->seconds_total = secs;

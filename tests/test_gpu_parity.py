@@ -234,6 +234,17 @@ def test_upload_inconsistent_then_run(orc, strategy):
         assert eng.download().tobytes() == want.tobytes()
 
 
+def test_long_stream_run_is_chunked(orc):
+    """A run longer than one graph (1024 steps) goes through several graphs."""
+    cfg = fsb.baseline_config(20_000, 2500)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "stream") as eng:
+        trace, _, _ = eng.simulate(barycentre=False)
+        assert eng.last_launches() == 2500 + 3  # 3 graphs, each with its trailing eat
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == want_fish.tobytes()
+
+
 def test_run_split_equals_whole(orc):
     cfg = fsb.baseline_config(40_000, 12)
     with make(cfg, "stream") as a, make(cfg, "stream") as b:
