@@ -28,6 +28,9 @@ VARIANTS = {
     "b1s4m3": ["-DFSB_BULK_PAIRS=1", "-DFSB_BULK_STAGES=4", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b4s2m1": ["-DFSB_BULK_PAIRS=4", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=1"],
+    # RNG high-word shifts on the fma pipe (IMAD.HI) instead of the alu pipe
+    "imadsh": ["-DFSB_IMAD_SHIFTS=1"],
+    "imadsh_p2b3": ["-DFSB_IMAD_SHIFTS=1", "-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=3"],
     # LDG kernel, one fish per thread
     "single4": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=4"],
     "single6": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=6"],
