@@ -239,7 +239,7 @@ def run_ours(args, world, rank, local):
     n_total = n_local * world
     cfg = fsb.baseline_config(n_total, args.warmup + args.steps)
     uid = None
-    if world > 1:
+    if world > 1 and not args.peer:
         import torch.distributed as dist
 
         obj = [fsb.nccl_unique_id() if rank == 0 else None]
@@ -249,7 +249,13 @@ def run_ours(args, world, rank, local):
         uid = fsb.nccl_unique_id()
     eng = fsb.Engine(cfg, device=local, rank=rank, world_size=world, nccl_unique_id=uid,
                      strategy=args.strategy, alternate=not args.no_alternate, bulk=not args.no_bulk,
-                     force_nccl=args.force_nccl)
+                     force_nccl=args.force_nccl, peer=args.peer)
+    if args.peer and world > 1:
+        import torch.distributed as dist
+
+        handles = [None] * world
+        dist.all_gather_object(handles, eng.peer_handle())
+        eng.peer_connect(handles)
     eng.init()
     if args.warmup:
         eng.run(0, args.warmup)
@@ -368,6 +374,8 @@ def main():
                     help="LDG step kernel instead of the cp.async.bulk shared-memory ring")
     ap.add_argument("--force-nccl", action="store_true",
                     help="exercise the NCCL exchange path even on one rank (testing)")
+    ap.add_argument("--peer", action="store_true",
+                    help="per-step exchange by NVLink peer stores from the step kernel instead of NCCL")
     ap.add_argument("--cpu-steps", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

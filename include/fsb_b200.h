@@ -79,6 +79,8 @@ enum fsb_strategy {
 #define FSB_FLAG_NO_BULK 0x4u      /* step kernel loads with LDG instead of the cp.async.bulk smem ring */
 #define FSB_FLAG_FORCE_BULK 0x8u   /* bulk ring even for schools too small to amortise it (testing) */
 #define FSB_FLAG_NO_PDL 0x10u      /* no Programmatic Dependent Launch between graph step kernels */
+#define FSB_FLAG_PEER_EXCHANGE 0x20u /* per-step exchange by NVLink peer stores from the step kernel
+                                        itself (CUDA IPC windows) instead of an NCCL allgather */
 
 typedef struct fsb_engine_options {
     int device;                  /* CUDA device ordinal of this shard */
@@ -173,6 +175,15 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
 
 /* Kernel launch count of the last fsb_engine_run (for bench accounting). */
 int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches);
+
+/* Peer exchange (FSB_FLAG_PEER_EXCHANGE, one process per GPU): each rank
+ * exports its 64-byte CUDA IPC handle of its exchange window, the caller
+ * all-gathers the handles (rank order) and every rank connects.  The step
+ * kernel's last CTA then writes the rank partial into every peer window over
+ * NVLink and releases an epoch flag; the next step's kernel acquires the flags.
+ * A single rank connects to itself at creation. */
+int fsb_engine_peer_handle(fsb_engine* e, void* out, size_t len);
+int fsb_engine_peer_connect(fsb_engine* e, const void* handles, size_t len);
 
 /* Device self-test of the guarded fast fp64 paths the step kernel uses
  * (fsb_math.cuh): n generated operands (raw bit patterns incl. NaN, inf,

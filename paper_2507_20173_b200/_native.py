@@ -28,6 +28,7 @@ FLAG_FORCE_NCCL = 0x2
 FLAG_NO_BULK = 0x4
 FLAG_FORCE_BULK = 0x8
 FLAG_NO_PDL = 0x10
+FLAG_PEER_EXCHANGE = 0x20
 
 
 class fsb_sim_config(ctypes.Structure):
@@ -90,6 +91,8 @@ SIGNATURES = [
     ("fsb_engine_stream", _int, [_vp, _P(_vp)]),
     ("fsb_engine_time_step_kernels", _int, [_vp, _u64, _u64, _vp]),
     ("fsb_engine_last_launches", _int, [_vp, _P(_u64)]),
+    ("fsb_engine_peer_handle", _int, [_vp, _vp, _sz]),
+    ("fsb_engine_peer_connect", _int, [_vp, _vp, _sz]),
     ("fsb_selftest_fast_math", _int, [_int, _u64, _u64, _vp]),
 ]
 

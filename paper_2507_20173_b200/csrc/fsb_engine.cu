@@ -130,8 +130,8 @@ struct fsb_engine {
     Partial* part_all = nullptr;  // [2][world]
     Partial* block_part = nullptr;
     unsigned* counter = nullptr;
-    uint64_t* d_step0 = nullptr;
-    uint64_t* h_step0 = nullptr;  // pinned
+    uint64_t* d_step0 = nullptr;  // [2]: first step of the launched graph, exchange epoch base
+    uint64_t* h_step0 = nullptr;  // pinned [2], copied by each graph's first node
     double* d_scalar = nullptr;   // [4]
     int* d_mismatch = nullptr;
     int grid = 0;            // grid of the compact-state step kernel in use
@@ -147,6 +147,14 @@ struct fsb_engine {
 
     std::map<std::pair<uint64_t, int>, GraphEntry> graphs;
     ncclComm_t comm = nullptr;
+
+    // peer exchange (FSB_FLAG_PEER_EXCHANGE)
+    bool peer_mode = false;
+    bool peer_connected = false;
+    fsb_dev::PeerWindow* window = nullptr;   // this rank's window (IPC-exported)
+    fsb_dev::PeerWindow** d_peers = nullptr;  // [world] device array of mapped windows
+    std::vector<void*> opened;               // IPC mappings to close
+    uint64_t xseq = 0;                       // exchanges completed (epoch of the latest)
 };
 
 namespace {
@@ -198,8 +206,28 @@ int elapsed(fsb_engine* e, double* seconds) {
     return FSB_OK;
 }
 
+// The kernels' view of the peer exchange: epochs base + in_add / base + out_add
+// with base = *seq_ptr (graph) or 0 (eager launches pass absolute epochs).
+fsb_dev::PeerXchg px_of(const fsb_engine* e, const uint64_t* seq_ptr, uint64_t in_add, uint64_t out_add) {
+    fsb_dev::PeerXchg px{};
+    if (!e->peer_mode) return px;
+    px.peers = e->d_peers;
+    px.local = e->window;
+    px.rank = e->rank;
+    px.seq_ptr = seq_ptr;
+    px.in_add = in_add;
+    px.out_add = out_add;
+    return px;
+}
+
+int need_peers(const fsb_engine* e) {
+    if (e->peer_mode && !e->peer_connected)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "peer exchange not connected (fsb_engine_peer_connect)");
+    return FSB_OK;
+}
+
 bool want_persistent(const fsb_engine* e) {
-    if (e->world != 1 || e->use_nccl) return false;
+    if (e->world != 1 || e->use_nccl || e->peer_mode) return false;
     if (e->strategy == FSB_STRATEGY_PERSISTENT) return true;
     if (e->strategy == FSB_STRATEGY_STREAM) return false;
     return e->count > 0 && e->count <= 16384;
@@ -243,7 +271,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
     CU(cudaMalloc(&g.d_bary, 3 * T * sizeof(double)));
     CU(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
     int rc = FSB_OK;
-    cudaError_t ce = cudaMemcpyAsync(e->d_step0, e->h_step0, sizeof(uint64_t), cudaMemcpyHostToDevice,
+    cudaError_t ce = cudaMemcpyAsync(e->d_step0, e->h_step0, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                      e->stream);
     uint64_t launches = 0;
     for (uint64_t k = 0; k < T && ce == cudaSuccess && rc == FSB_OK; ++k) {
@@ -256,6 +284,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         a.trace_out = k ? g.d_trace + (k - 1) : nullptr;
         a.bary_out = k ? g.d_bary + 3 * (k - 1) : nullptr;
         a.part_out = local_part(e, (int)(k & 1));
+        a.px = px_of(e, e->d_step0 + 1, k, k + 1);  // consumes epoch base+k, produces base+k+1
         a.pdl = (k > 0 && use_pdl(e)) ? 1 : 0;  // kernel -> kernel edges only
         ce = fsb_dev::launch_step(a, (k == 0 && explicit_first) ? e->grid_explicit : e->grid, e->stream);
         ++launches;
@@ -271,6 +300,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         ea.world = e->world;
         ea.trace_out = g.d_trace + (T - 1);
         ea.bary_out = g.d_bary + 3 * (T - 1);
+        ea.px = px_of(e, e->d_step0 + 1, T, 0);
         ea.pdl = use_pdl(e) ? 1 : 0;
         ce = fsb_dev::launch_eat(ea, e->grid, e->stream);
         ++launches;
@@ -298,7 +328,8 @@ int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, do
         TRY(build_graph(e, T, e->cur_explicit, &g));
         it = e->graphs.emplace(key, g).first;
     }
-    *e->h_step0 = first_step;
+    e->h_step0[0] = first_step;
+    e->h_step0[1] = e->xseq;  // exchange epoch base of this launch
     CU(cudaEventRecord(e->ev0, e->stream));
     CU(cudaGraphLaunch(it->second.exec, e->stream));
     CU(cudaEventRecord(e->ev1, e->stream));
@@ -310,6 +341,7 @@ int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, do
     e->max_valid = e->sums_valid = true;
     e->cur_buf = (int)((T - 1) & 1);
     e->last_launches = it->second.launches;
+    e->xseq += T;  // one exchange per step kernel
     return FSB_OK;
 }
 
@@ -360,23 +392,38 @@ int reduce_current(fsb_engine* e) {
     a.ws.block_part = e->block_part;
     a.ws.counter = e->counter;
     a.part_out = local_part(e, 0);
-    if (e->count == 0) {
-        const Partial id{-INFINITY, 0.0, 0.0, 0.0};
-        CU(cudaMemcpyAsync(a.part_out, &id, sizeof(Partial), cudaMemcpyHostToDevice, e->stream));
-    } else {
-        CU(fsb_dev::launch_reduce(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
-    }
+    a.world = e->world;
+    a.px = px_of(e, nullptr, 0, e->xseq + 1);
+    // launched even for an empty shard: it publishes the identity partial (and,
+    // with a peer exchange, pushes it so the other ranks are not kept waiting)
+    CU(fsb_dev::launch_reduce(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
     TRY(exchange(e, 0));
     e->cur_buf = 0;
     e->max_valid = e->sums_valid = true;
+    e->xseq += 1;
     return FSB_OK;
 }
 
 int host_combine(fsb_engine* e, Partial* out) {
     std::vector<Partial> parts(e->world);
-    CU(cudaMemcpyAsync(parts.data(), all_part(e, e->cur_buf), e->world * sizeof(Partial),
-                       cudaMemcpyDeviceToHost, e->stream));
-    CU(cudaStreamSynchronize(e->stream));
+    if (e->peer_mode) {
+        // the latest epoch's slots, once every rank's flag shows it has landed
+        const int b = (int)(e->xseq & 1);
+        std::vector<unsigned long long> flags(e->world);
+        for (int spins = 0;; ++spins) {
+            CU(cudaMemcpy(flags.data(), &e->window->flags[b][0], e->world * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost));
+            bool all = true;
+            for (unsigned long long f : flags) all = all && f == e->xseq;
+            if (all) break;
+            if (spins > 20000000) return fail(FSB_ERR_NCCL, "peer exchange: timed out waiting for ranks");
+        }
+        CU(cudaMemcpy(parts.data(), &e->window->slots[b][0], e->world * sizeof(Partial), cudaMemcpyDeviceToHost));
+    } else {
+        CU(cudaMemcpyAsync(parts.data(), all_part(e, e->cur_buf), e->world * sizeof(Partial),
+                           cudaMemcpyDeviceToHost, e->stream));
+        CU(cudaStreamSynchronize(e->stream));
+    }
     // rank order, same operators as the device combine (no contraction: adds only)
     Partial r{-INFINITY, 0.0, 0.0, 0.0};
     for (const Partial& p : parts) {
@@ -468,6 +515,9 @@ int fsb_engine_destroy(fsb_engine* e) {
     if (e->stream) cudaStreamSynchronize(e->stream);
     free_graphs(e);
     if (e->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(e->comm);
+    for (void* p : e->opened) cudaIpcCloseMemHandle(p);
+    if (e->window) cudaFree(e->window);
+    if (e->d_peers) cudaFree(e->d_peers);
     for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
                     (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
                     (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
@@ -514,7 +564,8 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     e->world = o.world_size;
     e->strategy = o.strategy;
     e->flags = o.flags;
-    e->use_nccl = o.world_size > 1 || (o.flags & FSB_FLAG_FORCE_NCCL);
+    e->peer_mode = (o.flags & FSB_FLAG_PEER_EXCHANGE) != 0;
+    e->use_nccl = !e->peer_mode && (o.world_size > 1 || (o.flags & FSB_FLAG_FORCE_NCCL));
     fsb_shard_range(cfg->num_fish, e->world, e->rank, &e->first, &e->count);
 
     auto bail = [&](int rc) {
@@ -554,8 +605,18 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
     CB(cudaMalloc(&e->counter, sizeof(unsigned)));
     CB(cudaMemset(e->counter, 0, sizeof(unsigned)));
-    CB(cudaMalloc(&e->d_step0, sizeof(uint64_t)));
-    CB(cudaMallocHost(&e->h_step0, sizeof(uint64_t)));
+    CB(cudaMalloc(&e->d_step0, 2 * sizeof(uint64_t)));
+    CB(cudaMallocHost(&e->h_step0, 2 * sizeof(uint64_t)));
+    if (e->peer_mode) {
+        if (e->world > fsb_dev::kMaxRanks) return bail(fail(FSB_ERR_UNSUPPORTED, "peer exchange: too many ranks"));
+        CB(cudaMalloc(&e->window, sizeof(fsb_dev::PeerWindow)));
+        CB(cudaMemset(e->window, 0, sizeof(fsb_dev::PeerWindow)));
+        CB(cudaMalloc(&e->d_peers, e->world * sizeof(fsb_dev::PeerWindow*)));
+        if (e->world == 1) {  // a single rank exchanges with itself
+            CB(cudaMemcpy(e->d_peers, &e->window, sizeof(fsb_dev::PeerWindow*), cudaMemcpyHostToDevice));
+            e->peer_connected = true;
+        }
+    }
     CB(cudaMalloc(&e->d_scalar, 4 * sizeof(double)));
     CB(cudaMalloc(&e->d_mismatch, sizeof(int)));
 
@@ -640,13 +701,15 @@ int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count) {
 
 int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
     TRY(guard(e));
+    TRY(need_peers(e));
     CU(cudaEventRecord(e->ev0, e->stream));
-    if (e->count) {
+    if (e->count || e->peer_mode) {  // an empty shard still publishes (and pushes) its identity partial
         fsb_dev::StepArgs a = step_args(e, canonical(e));
         a.step_ptr = nullptr;
         a.step_add = step;
         a.part_in = nullptr;  // no pending eat: phases are applied eagerly
         a.part_out = local_part(e, 0);
+        a.px = px_of(e, nullptr, 0, e->xseq + 1);
         CU(fsb_dev::launch_step(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
     } else {
         const Partial id{-INFINITY, 0.0, 0.0, 0.0};
@@ -658,11 +721,13 @@ int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
     e->cur_explicit = false;
     e->max_valid = e->sums_valid = true;
     e->cur_buf = 0;
+    e->xseq += 1;
     return FSB_OK;
 }
 
 int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     TRY(guard(e));
+    TRY(need_peers(e));
     CU(cudaEventRecord(e->ev0, e->stream));
     if (!e->max_valid) TRY(reduce_current(e));
     fsb_dev::EatArgs a{};
@@ -671,6 +736,7 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     a.n = e->count;
     a.part_in = all_part(e, e->cur_buf);
     a.world = e->world;
+    a.px = px_of(e, nullptr, e->xseq, 0);
     a.trace_out = e->d_scalar;
     CU(fsb_dev::launch_eat(a, e->grid, e->stream));
     CU(cudaEventRecord(e->ev1, e->stream));
@@ -705,10 +771,11 @@ int run_stream_chunked(fsb_engine* e, uint64_t first_step, uint64_t T, double* t
 int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* trace, double* bary,
                    fsb_timing* timing) {
     TRY(guard(e));
+    TRY(need_peers(e));
     if (timing) *timing = fsb_timing{0.0, 0.0, 0.0};
     if (num_steps == 0) return FSB_OK;
     double secs = 0.0;
-    if (e->count == 0 && !e->use_nccl) {
+    if (e->count == 0 && !e->use_nccl && !e->peer_mode) {
         // empty school: every max is -inf (executor.hpp:86), sums are 0
         for (uint64_t k = 0; k < num_steps; ++k) {
             if (trace) trace[k] = -INFINITY;
@@ -749,6 +816,7 @@ int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* 
 
 int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
     TRY(guard(e));
+    TRY(need_peers(e));
     if (!e->max_valid || !e->sums_valid) TRY(reduce_current(e));
     Partial r;
     TRY(host_combine(e, &r));
@@ -817,19 +885,22 @@ int fsb_engine_stream(fsb_engine* e, void** stream) {
 
 int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* kernel_ms) {
     TRY(guard(e));
+    TRY(need_peers(e));
     if (!kernel_ms && num_steps) return fail(FSB_ERR_INVALID_ARGUMENT, "null kernel_ms");
-    if (e->count == 0) {
+    if (e->count == 0 && e->world == 1) {
         for (uint64_t k = 0; k < num_steps; ++k) kernel_ms[k] = 0.0;
         return FSB_OK;
     }
     std::vector<cudaEvent_t> ev(num_steps + 1);
     for (auto& v : ev) CU(cudaEventCreate(&v));
     CU(cudaEventRecord(ev[0], e->stream));
+    const uint64_t x0 = e->xseq;
     for (uint64_t k = 0; k < num_steps; ++k) {
         fsb_dev::StepArgs a = step_args(e, canonical(e));
         a.step_add = first_step + k;
         a.part_in = (k == 0) ? nullptr : all_part(e, (int)((k - 1) & 1));
         a.part_out = local_part(e, (int)(k & 1));
+        a.px = px_of(e, nullptr, k ? x0 + k : 0, x0 + k + 1);
         CU(fsb_dev::launch_step(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
         e->cur_explicit = false;
         CU(cudaEventRecord(ev[k + 1], e->stream));
@@ -843,9 +914,11 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
         ea.n = e->count;
         ea.part_in = all_part(e, (int)((num_steps - 1) & 1));
         ea.world = e->world;
+        ea.px = px_of(e, nullptr, x0 + num_steps, 0);
         CU(fsb_dev::launch_eat(ea, e->grid, e->stream));
         e->cur_buf = (int)((num_steps - 1) & 1);
         e->max_valid = e->sums_valid = true;
+        e->xseq = x0 + num_steps;
     }
     CU(cudaStreamSynchronize(e->stream));
     for (uint64_t k = 0; k < num_steps; ++k) {
@@ -882,5 +955,38 @@ extern "C" int fsb_selftest_fast_math(int device, uint64_t n, uint64_t seed, uin
     cudaFree(d);
     if (e != cudaSuccess) return cuda_fail(e, "selftest fast math");
     for (int k = 0; k < 4; ++k) out[k] = h[k];
+    return FSB_OK;
+}
+
+extern "C" int fsb_engine_peer_handle(fsb_engine* e, void* out, size_t len) {
+    TRY(guard(e));
+    if (!e->peer_mode) return fail(FSB_ERR_INVALID_ARGUMENT, "engine not created with FSB_FLAG_PEER_EXCHANGE");
+    if (!out || len < sizeof(cudaIpcMemHandle_t)) return fail(FSB_ERR_INVALID_ARGUMENT, "need 64 bytes");
+    cudaIpcMemHandle_t h;
+    CU(cudaIpcGetMemHandle(&h, e->window));
+    std::memcpy(out, &h, sizeof h);
+    return FSB_OK;
+}
+
+extern "C" int fsb_engine_peer_connect(fsb_engine* e, const void* handles, size_t len) {
+    TRY(guard(e));
+    if (!e->peer_mode) return fail(FSB_ERR_INVALID_ARGUMENT, "engine not created with FSB_FLAG_PEER_EXCHANGE");
+    const size_t hs = sizeof(cudaIpcMemHandle_t);
+    if (!handles || len < hs * (size_t)e->world) return fail(FSB_ERR_INVALID_ARGUMENT, "need world_size handles");
+    std::vector<fsb_dev::PeerWindow*> peers(e->world);
+    for (int q = 0; q < e->world; ++q) {
+        if (q == e->rank) {
+            peers[q] = e->window;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, static_cast<const char*>(handles) + hs * q, hs);
+        void* p = nullptr;
+        CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        e->opened.push_back(p);
+        peers[q] = static_cast<fsb_dev::PeerWindow*>(p);
+    }
+    CU(cudaMemcpy(e->d_peers, peers.data(), e->world * sizeof(fsb_dev::PeerWindow*), cudaMemcpyHostToDevice));
+    e->peer_connected = true;
     return FSB_OK;
 }

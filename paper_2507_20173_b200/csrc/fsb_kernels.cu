@@ -129,9 +129,67 @@ __device__ __forceinline__ void store_partial(Partial* p, const Partial& v) {
     q[1] = make_double2(v.sy, v.sf);
 }
 
+__device__ __forceinline__ uint64_t epoch_of(const PeerXchg& px, uint64_t add) {
+    return add ? (px.seq_ptr ? *px.seq_ptr : 0ull) + add : 0ull;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ double ld_relaxed_sys(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Peer exchange, producer side (warp 0 of the last CTA): the rank partial into
+// every peer's window, then the epoch flag with release semantics.
+__device__ __forceinline__ void push_to_peers(const PeerXchg& px, int world, uint64_t epoch, const Partial& tot) {
+    const int b = (int)(epoch & 1);
+    for (int q = threadIdx.x; q < world; q += 32) {
+        PeerWindow* w = px.peers[q];
+        store_partial(&w->slots[b][px.rank], tot);
+        __threadfence_system();
+        st_release_sys(&w->flags[b][px.rank], epoch);
+    }
+}
+
+// Peer exchange, consumer side (every CTA): thread 0 acquires the epoch's
+// flags of all ranks from the local window, then every thread combines the
+// slots in rank order.
+__device__ __forceinline__ Partial wait_and_combine_peers(const PeerXchg& px, int world, uint64_t epoch) {
+    __shared__ Partial combined;
+    const int b = (int)(epoch & 1);
+    PeerWindow* w = px.local;
+    if (threadIdx.x == 0) {
+        Partial r = identity();
+        for (int q = 0; q < world; ++q) {
+            while (ld_acquire_sys(&w->flags[b][q]) != epoch) __nanosleep(64);
+            Partial v;
+            v.best = ld_relaxed_sys(&w->slots[b][q].best);
+            v.sx = ld_relaxed_sys(&w->slots[b][q].sx);
+            v.sy = ld_relaxed_sys(&w->slots[b][q].sy);
+            v.sf = ld_relaxed_sys(&w->slots[b][q].sf);
+            fold(r, v);
+        }
+        combined = r;
+    }
+    __syncthreads();
+    return combined;
+}
+
 // CTA partial -> global; the last CTA to arrive combines all CTA partials in
-// index order and publishes this rank's partial.
-__device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs& ws, Partial* part_out) {
+// index order and publishes this rank's partial (and, with a peer exchange,
+// pushes it to every rank).
+__device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs& ws, Partial* part_out,
+                                            const PeerXchg& px, int world) {
     __shared__ Partial scratch[32];
     __shared__ bool am_last;
     const Partial blk = block_reduce(local, scratch);
@@ -152,6 +210,8 @@ __device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs
         store_partial(part_out, tot);
         *ws.counter = 0u;  // ready for the next launch
     }
+    const uint64_t epoch = px.peers ? epoch_of(px, px.out_add) : 0ull;
+    if (epoch && threadIdx.x < 32) push_to_peers(px, world, epoch, tot);
 }
 
 // Programmatic Dependent Launch: block until the predecessor grid has completed
@@ -162,8 +222,13 @@ __device__ __forceinline__ void pdl_wait_and_release() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Combine the ranks' partials of the previous step in rank order.
-__device__ __forceinline__ Partial combine_ranks(const Partial* part_in, int world) {
+// Combine the ranks' partials of the previous step in rank order: from
+// part_in (single rank / NCCL allgather) or from the peer window.
+__device__ __forceinline__ Partial combine_prev(const Partial* part_in, int world, const PeerXchg& px) {
+    if (px.peers) {
+        const uint64_t epoch = epoch_of(px, px.in_add);
+        return epoch ? wait_and_combine_peers(px, world, epoch) : identity();
+    }
     Partial r = identity();
     if (part_in) {
         for (int k = 0; k < world; ++k) fold(r, part_in[k]);
@@ -315,7 +380,7 @@ template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
     const StepParams P = params_of(a.k);
     pdl_wait_and_release();
-    const Partial prev = combine_ranks(a.part_in, a.world);
+    const Partial prev = combine_prev(a.part_in, a.world, a.px);
     publish_prev(prev, a.trace_out, a.bary_out);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
@@ -388,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
         a.s.w[i] = w;
         a.s.p[i] = p;
     }
-    grid_finish(acc, a.ws, a.part_out);
+    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 
 // ---------------------------------------------------------------------------
@@ -461,7 +526,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
 
     const StepParams P = params_of(a.k);
     pdl_wait_and_release();
-    const Partial prev = combine_ranks(a.part_in, a.world);
+    const Partial prev = combine_prev(a.part_in, a.world, a.px);
     publish_prev(prev, a.trace_out, a.bary_out);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
@@ -578,7 +643,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
             a.s.p[i] = p;
         }
     }
-    grid_finish(acc, a.ws, a.part_out);
+    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 
 #if FSB_SINGLE
@@ -587,7 +652,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
 __global__ void __launch_bounds__(kThreads, FSB_SINGLE_MIN_BLOCKS) step_kernel_single(const StepArgs a) {
     const StepParams P = params_of(a.k);
     pdl_wait_and_release();
-    const Partial prev = combine_ranks(a.part_in, a.world);
+    const Partial prev = combine_prev(a.part_in, a.world, a.px);
     publish_prev(prev, a.trace_out, a.bary_out);
     const bool eat = prev.best > 0.0;
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
@@ -633,14 +698,14 @@ __global__ void __launch_bounds__(kThreads, FSB_SINGLE_MIN_BLOCKS) step_kernel_s
             a.s.p[i] = p;
         }
     }
-    grid_finish(acc, a.ws, a.part_out);
+    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 #endif
 
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
     pdl_wait_and_release();
-    const Partial prev = combine_ranks(a.part_in, a.world);
+    const Partial prev = combine_prev(a.part_in, a.world, a.px);
     publish_prev(prev, a.trace_out, a.bary_out);
     if (!(prev.best > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
     const SharedDivisor M = make_divisor(prev.best);
@@ -687,7 +752,7 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceArgs a) {
         const double cur = kExplicitCur ? a.s.c[i] : objective(x, y, half);
         accumulate(acc, x, y, a.s.p[i], cur);
     }
-    grid_finish(acc, a.ws, a.part_out);
+    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 
 struct FishAoS {

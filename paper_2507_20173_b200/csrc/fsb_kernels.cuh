@@ -99,6 +99,29 @@ struct ReduceWs {
     unsigned* counter;    // zero between launches
 };
 
+// Peer exchange (FSB_FLAG_PEER_EXCHANGE): every rank owns one window in its
+// HBM, exported with CUDA IPC and mapped by every peer.  The last CTA of a
+// rank's step kernel stores the rank partial straight into slot [epoch&1][rank]
+// of every peer's window over NVLink and then releases flag [epoch&1][rank] =
+// epoch (system scope); the next kernel on each rank acquires all flags of the
+// epoch from its own window and combines the slots in rank order.  Epochs are a
+// per-engine exchange sequence number, identical on all ranks.
+constexpr int kMaxRanks = 64;
+
+struct PeerWindow {
+    Partial slots[2][kMaxRanks];
+    unsigned long long flags[2][kMaxRanks];
+};
+
+struct PeerXchg {
+    PeerWindow* const* peers;  // device array [world]: peer windows as mapped here (nullptr = off)
+    PeerWindow* local;         // this rank's window
+    int rank;
+    const uint64_t* seq_ptr;   // epoch base = (seq_ptr ? *seq_ptr : 0) ...
+    uint64_t in_add;           // ... + in_add: epoch of the partials consumed (0 = none)
+    uint64_t out_add;          // ... + out_add: epoch of the partial produced (0 = none)
+};
+
 struct StepArgs {
     SoA s;
     Scalars k;
@@ -115,6 +138,7 @@ struct StepArgs {
     int alternate;        // reverse tile order on odd steps (L2 reuse across steps)
     int bulk;             // stream through shared memory with cp.async.bulk (compact state)
     int pdl;              // launched as a programmatic dependent of the previous step
+    PeerXchg px;          // peer exchange instead of part_in/part_out (px.peers != nullptr)
 };
 
 struct EatArgs {
@@ -126,6 +150,7 @@ struct EatArgs {
     double* trace_out;
     double* bary_out;
     int pdl;
+    PeerXchg px;
 };
 
 struct ReduceArgs {
@@ -134,6 +159,8 @@ struct ReduceArgs {
     uint64_t n;
     ReduceWs ws;
     Partial* part_out;
+    PeerXchg px;
+    int world;
 };
 
 struct InitArgs {

@@ -133,13 +133,14 @@ class Engine:
 
     def __init__(self, cfg: SimConfig, device: int = 0, rank: int = 0, world_size: int = 1,
                  nccl_unique_id: Optional[bytes] = None, strategy: str = "auto",
-                 alternate: bool = True, force_nccl: bool = False, bulk=True, pdl: bool = True):
+                 alternate: bool = True, force_nccl: bool = False, bulk=True, pdl: bool = True,
+                 peer: bool = False):
         self.cfg = cfg
         L = N.lib()
         self._uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
         flags = ((0 if alternate else N.FLAG_NO_ALTERNATE) | (N.FLAG_FORCE_NCCL if force_nccl else 0)
                  | (0 if bulk else N.FLAG_NO_BULK) | (N.FLAG_FORCE_BULK if bulk == "force" else 0)
-                 | (0 if pdl else N.FLAG_NO_PDL))
+                 | (0 if pdl else N.FLAG_NO_PDL) | (N.FLAG_PEER_EXCHANGE if peer else 0))
         opts = N.fsb_engine_options(device, rank, world_size,
                                     ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
                                     STRATEGIES[strategy], flags)
@@ -218,6 +219,17 @@ class Engine:
         xy = np.empty(2, dtype=np.float64)
         N.check(N.lib().fsb_engine_barycentre(self._h, _ptr(sums), _ptr(xy)))
         return sums, xy
+
+    def peer_handle(self) -> bytes:
+        """This rank's 64-byte IPC handle (peer exchange engines)."""
+        buf = ctypes.create_string_buffer(64)
+        N.check(N.lib().fsb_engine_peer_handle(self._h, buf, 64))
+        return buf.raw
+
+    def peer_connect(self, handles) -> None:
+        """Map every rank's window; `handles` = all ranks' peer_handle() in rank order."""
+        blob = b"".join(handles)
+        N.check(N.lib().fsb_engine_peer_connect(self._h, blob, len(blob)))
 
     def gather(self, local_idx) -> np.ndarray:
         """Fish at the given shard-local indices (Fish layout)."""

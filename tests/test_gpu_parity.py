@@ -304,6 +304,32 @@ def test_force_nccl_world1(orc):
         assert bits(eng.eat().max_diff) == bits(orc.eat(ocfg(cfg), want_fish))
 
 
+@pytest.mark.parametrize("n,t", [(100_001, 9), (4096, 30), (1, 5), (0, 3)])
+def test_peer_exchange_world1(orc, n, t):
+    """FSB_FLAG_PEER_EXCHANGE on one rank: the step kernel pushes its partial
+    into the (self-mapped) peer window and the next kernel acquires the epoch
+    flag -- the same code path the NVLink exchange takes across GPUs."""
+    cfg = fsb.baseline_config(n, t)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "auto", peer=True) as eng:
+        trace, bary, _ = eng.simulate(barycentre=True)
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == want_fish.tobytes()
+        if n:
+            assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
+            sums, _ = eng.barycentre()
+            assert rel_ok(sums, orc.barycentre_sums(want_fish))
+        # phases and the eager per-kernel timing path advance the same epochs
+        eng.move(t)
+        orc.move(ocfg(cfg), t, want_fish)
+        assert bits(eng.eat().max_diff) == bits(orc.eat(ocfg(cfg), want_fish))
+        eng.time_step_kernels(t + 1, 3)
+        orc.run(ocfg(cfg), want_fish, t + 1, 3)
+        tr, _, _ = eng.run(t + 4, 2)
+        assert tr.tobytes() == orc.run(ocfg(cfg), want_fish, t + 4, 2).tobytes()
+        assert eng.download().tobytes() == want_fish.tobytes()
+
+
 @pytest.mark.parametrize("name", ["C0_1e6x100", "C1_1e7x100", "C4_4096x100000", "C2_1e8x50"])
 def test_baseline_configs_match_reference_digests(golden_baseline, orc, name):
     if name not in golden_baseline:
