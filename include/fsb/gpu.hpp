@@ -193,6 +193,16 @@ class Engine {
         check(fsb_engine_checksum(e_.get(), h, &out));
         return out;
     }
+    // Peer exchange (Options::flags |= FSB_FLAG_PEER_EXCHANGE): this rank's IPC
+    // handle, and connecting with every rank's handle in rank order.
+    std::vector<unsigned char> peer_handle() {
+        std::vector<unsigned char> h(64);
+        check(fsb_engine_peer_handle(e_.get(), h.data(), h.size()));
+        return h;
+    }
+    void peer_connect(const std::vector<unsigned char>& all_handles) {
+        check(fsb_engine_peer_connect(e_.get(), all_handles.data(), all_handles.size()));
+    }
 
   private:
     struct Del {
