@@ -70,7 +70,9 @@ typedef struct fsb_timing {
 enum fsb_strategy {
     FSB_STRATEGY_AUTO = 0,       /* persistent for small single-GPU schools, else stream */
     FSB_STRATEGY_STREAM = 1,     /* one fused step kernel per step, CUDA-graph replayed  */
-    FSB_STRATEGY_PERSISTENT = 2  /* one thread-block cluster runs all steps on chip       */
+    FSB_STRATEGY_PERSISTENT = 2, /* one thread-block cluster runs all steps on chip       */
+    FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps,
+                                    a grid barrier per step (single GPU, mid-size schools) */
 };
 
 /* Engine flags. */

@@ -22,6 +22,7 @@ FSB_ERR_UNSUPPORTED = 6
 STRATEGY_AUTO = 0
 STRATEGY_STREAM = 1
 STRATEGY_PERSISTENT = 2
+STRATEGY_GRID = 3
 
 FLAG_NO_ALTERNATE = 0x1
 FLAG_FORCE_NCCL = 0x2

@@ -136,6 +136,9 @@ struct fsb_engine {
     int* d_mismatch = nullptr;
     int grid = 0;            // grid of the compact-state step kernel in use
     int grid_explicit = 0;   // grid of the explicit-cur step kernel
+    int grid_coop = 0;       // grid of the cooperative persistent grid kernel
+    Partial* d_combined = nullptr;           // [2] grid-kernel step partials
+    unsigned long long* d_gen = nullptr;     // grid-kernel generation word
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
 
     void* staging = nullptr;  // device AoS staging
@@ -345,6 +348,47 @@ int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, do
     return FSB_OK;
 }
 
+int ensure_run_buffers(fsb_engine* e, uint64_t T) {
+    if (T <= e->cl_cap) return FSB_OK;
+    if (e->d_cl_trace) cudaFree(e->d_cl_trace);
+    if (e->d_cl_bary) cudaFree(e->d_cl_bary);
+    e->d_cl_trace = e->d_cl_bary = nullptr;
+    e->cl_cap = 0;
+    CU(cudaMalloc(&e->d_cl_trace, T * sizeof(double)));
+    CU(cudaMalloc(&e->d_cl_bary, 3 * T * sizeof(double)));
+    e->cl_cap = T;
+    return FSB_OK;
+}
+
+// FSB_STRATEGY_GRID: one cooperative launch runs all T steps (compact state,
+// single rank), then the trace comes back.
+int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary, double* seconds) {
+    if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode)
+        return fail(FSB_ERR_UNSUPPORTED, "grid strategy: single rank, compact state only");
+    TRY(ensure_run_buffers(e, T));
+    fsb_dev::GridArgs g{};
+    g.base = step_args(e, canonical(e));
+    g.base.part_out = local_part(e, 0);
+    g.first_step = first_step;
+    g.num_steps = T;
+    g.trace = e->d_cl_trace;
+    g.bary = bary ? e->d_cl_bary : nullptr;
+    g.combined = e->d_combined;
+    g.gen = e->d_gen;
+    CU(cudaMemsetAsync(e->d_gen, 0, sizeof(unsigned long long), e->stream));
+    CU(cudaEventRecord(e->ev0, e->stream));
+    CU(fsb_dev::launch_grid_run(g, e->grid_coop, e->stream));
+    CU(cudaEventRecord(e->ev1, e->stream));
+    if (trace) CU(cudaMemcpyAsync(trace, e->d_cl_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    if (bary) CU(cudaMemcpyAsync(bary, e->d_cl_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    TRY(elapsed(e, seconds));
+    e->max_valid = e->sums_valid = true;
+    e->cur_buf = 0;
+    e->last_launches = 1;
+    return FSB_OK;
+}
+
 int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
                    double* seconds) {
     if (T > e->cl_cap) {
@@ -518,6 +562,8 @@ int fsb_engine_destroy(fsb_engine* e) {
     for (void* p : e->opened) cudaIpcCloseMemHandle(p);
     if (e->window) cudaFree(e->window);
     if (e->d_peers) cudaFree(e->d_peers);
+    for (void* p : {(void*)e->d_combined, (void*)e->d_gen})
+        if (p) cudaFree(p);
     for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
                     (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
                     (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
@@ -541,7 +587,7 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     if (opts) o = *opts;
     if (o.world_size < 1 || o.rank < 0 || o.rank >= o.world_size)
         return fail(FSB_ERR_INVALID_ARGUMENT, "bad rank/world_size");
-    if (o.strategy < FSB_STRATEGY_AUTO || o.strategy > FSB_STRATEGY_PERSISTENT)
+    if (o.strategy < FSB_STRATEGY_AUTO || o.strategy > FSB_STRATEGY_GRID)
         return fail(FSB_ERR_INVALID_ARGUMENT, "bad strategy");
 
     int ndev = 0;
@@ -600,7 +646,11 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
         e->grid = e->use_bulk ? grid_bulk : fsb_dev::step_grid_blocks(e->device, false, false);
     }
     e->grid_explicit = fsb_dev::step_grid_blocks(e->device, true, false);
-    const int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
+    e->grid_coop = fsb_dev::grid_kernel_blocks(e->device);
+    int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
+    if (e->grid_coop > maxgrid) maxgrid = e->grid_coop;
+    CB(cudaMalloc(&e->d_combined, 2 * sizeof(Partial)));
+    CB(cudaMalloc(&e->d_gen, sizeof(unsigned long long)));
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
     CB(cudaMalloc(&e->counter, sizeof(unsigned)));
@@ -786,6 +836,10 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
         e->max_valid = e->sums_valid = true;
         e->cur_buf = 0;
         e->last_launches = 0;
+    } else if (e->strategy == FSB_STRATEGY_GRID && !e->cur_explicit && e->world == 1 && !e->use_nccl &&
+               !e->peer_mode) {
+        // (the first run after an inconsistent upload takes the stream path below)
+        TRY(run_grid(e, first_step, num_steps, trace, bary, &secs));
     } else if (want_persistent(e)) {
         int rc = run_persistent(e, first_step, num_steps, trace, bary, &secs);
         if (rc == FSB_ERR_UNSUPPORTED && e->strategy == FSB_STRATEGY_AUTO)

@@ -149,6 +149,16 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 // Peer exchange, producer side (warp 0 of the last CTA): the rank partial into
 // every peer's window, then the epoch flag with release semantics.
 __device__ __forceinline__ void push_to_peers(const PeerXchg& px, int world, uint64_t epoch, const Partial& tot) {
@@ -376,16 +386,11 @@ __global__ void __launch_bounds__(kThreads) init_kernel(const InitArgs a) {
     }
 }
 
+// This CTA's share of one fused step (LDG path): its balanced chunk of pairs,
+// plus the odd tail fish on CTA 0.  Folds every fish into acc.
 template <bool kExplicitCur>
-__global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
-    const StepParams P = params_of(a.k);
-    pdl_wait_and_release();
-    const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out);
-    const bool eat = prev.best > 0.0;  // sim.hpp:115
-    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
-    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
-
+__device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& P, bool eat,
+                                           const SharedDivisor& M, uint64_t step, Partial& acc) {
     const uint64_t n = a.n;
     const uint64_t npairs = n >> 1;
     const bool rev = a.alternate && (step & 1ull);
@@ -407,7 +412,6 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
     double2* P2 = reinterpret_cast<double2*>(a.s.p);
     const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
 
-    Partial acc = identity();
     for (uint64_t j = 0; j < nsub; ++j) {
         const uint64_t sub = rev ? nsub - 1 - j : j;
         const uint64_t base = lo + sub * kTilePairs + threadIdx.x;
@@ -453,7 +457,94 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
         a.s.w[i] = w;
         a.s.p[i] = p;
     }
+}
+
+template <bool kExplicitCur>
+__global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
+    const StepParams P = params_of(a.k);
+    pdl_wait_and_release();
+    const Partial prev = combine_prev(a.part_in, a.world, a.px);
+    publish_prev(prev, a.trace_out, a.bary_out);
+    const bool eat = prev.best > 0.0;  // sim.hpp:115
+    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
+    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
+    Partial acc = identity();
+    step_chunk<kExplicitCur>(a, P, eat, M, step, acc);
     grid_finish(acc, a.ws, a.part_out, a.px, a.world);
+}
+
+// ---------------------------------------------------------------------------
+// grid_kernel: all T steps in ONE cooperative launch for mid-size schools
+// (the state stays in L2 between steps; no per-step launch).  Each step is
+// step_chunk on every CTA, then a grid barrier that is also the reduction:
+// the last CTA to arrive combines the CTA partials in index order, publishes
+// the step's partial and trace entry, and opens the next generation; the
+// others sleep on the generation word.  Co-residency of all CTAs is
+// guaranteed by the cooperative launch.
+__global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) grid_kernel(const GridArgs g) {
+    const StepArgs& a = g.base;
+    const StepParams P = params_of(a.k);
+    __shared__ Partial scratch[32];
+    __shared__ bool am_last;
+    __shared__ Partial shared_prev;
+    Partial prev = identity();  // no pending eat at the start of a run
+    for (uint64_t k = 0; k < g.num_steps; ++k) {
+        const uint64_t step = g.first_step + k;
+        const bool eat = prev.best > 0.0;
+        const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
+        Partial acc = identity();
+        step_chunk<false>(a, P, eat, M, step, acc);
+        const Partial blk = block_reduce(acc, scratch);
+        if (threadIdx.x == 0) {
+            store_partial(&a.ws.block_part[blockIdx.x], blk);
+            __threadfence();
+            am_last = atomicAdd(a.ws.counter, 1u) == gridDim.x - 1;
+        }
+        __syncthreads();
+        if (am_last) {
+            __threadfence();
+            Partial t = identity();
+            for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) fold(t, load_cg(&a.ws.block_part[i]));
+            __syncthreads();
+            const Partial tot = block_reduce(t, scratch);
+            if (threadIdx.x == 0) {
+                shared_prev = tot;
+                g.trace[k] = tot.best;
+                if (g.bary) {
+                    g.bary[3 * k + 0] = tot.sx;
+                    g.bary[3 * k + 1] = tot.sy;
+                    g.bary[3 * k + 2] = tot.sf;
+                }
+                store_partial(&g.combined[k & 1], tot);
+                *a.ws.counter = 0u;
+                __threadfence();
+                st_release_gpu(g.gen, k + 1);  // open generation k+1
+            }
+        } else if (threadIdx.x == 0) {
+            while (ld_acquire_gpu(g.gen) != k + 1) __nanosleep(32);
+            shared_prev = load_cg(&g.combined[k & 1]);
+        }
+        __syncthreads();
+        prev = shared_prev;
+        __syncthreads();  // shared_prev / scratch reuse by the next step
+    }
+    // trailing eat of the last step, on the fish this CTA itself updated
+    if (prev.best > 0.0 && g.num_steps) {
+        const SharedDivisor M = make_divisor(prev.best);
+        const uint64_t npairs = a.n >> 1;
+        constexpr uint64_t kAlign = 64;  // the chunk of step_chunk
+        const uint64_t nblk = (npairs + kAlign - 1) / kAlign;
+        const uint64_t lo = 2 * ((nblk * blockIdx.x / gridDim.x) * kAlign);
+        uint64_t hi = 2 * ((nblk * (blockIdx.x + 1) / gridDim.x) * kAlign);
+        if (hi > 2 * npairs) hi = 2 * npairs;
+        for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+            a.s.w[i] = eat_weight(a.s.w[i], a.s.p[i], objective(a.s.x[i], a.s.y[i], P.half_pond), M, P.w_max);
+        if ((a.n & 1ull) && blockIdx.x == 0 && threadIdx.x == 0) {
+            const uint64_t i = a.n - 1;
+            a.s.w[i] = eat_weight(a.s.w[i], a.s.p[i], objective(a.s.x[i], a.s.y[i], P.half_pond), M, P.w_max);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g.num_steps) store_partial(a.part_out, prev);
 }
 
 // ---------------------------------------------------------------------------
@@ -1039,6 +1130,22 @@ cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st) {
     const bool pdl = a.pdl != 0;
     if (a.s.c) return launch_maybe_pdl(eat_kernel<true>, grid, kThreads, 0, st, a, pdl);
     return launch_maybe_pdl(eat_kernel<false>, grid, kThreads, 0, st, a, pdl);
+}
+
+int grid_kernel_blocks(int device) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_kernel, kThreads, 0) != cudaSuccess ||
+        per_sm < 1) {
+        cudaGetLastError();
+        per_sm = 1;
+    }
+    return num_sms(device) * per_sm;
+}
+
+cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st) {
+    void* args[] = {const_cast<GridArgs*>(&g)};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(grid_kernel), dim3(grid), dim3(kThreads), args,
+                                       0, st);
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, int grid, cudaStream_t st) {

@@ -141,6 +141,18 @@ struct StepArgs {
     PeerXchg px;          // peer exchange instead of part_in/part_out (px.peers != nullptr)
 };
 
+// Persistent cooperative-grid run (FSB_STRATEGY_GRID): `base` supplies the
+// state, scalars and reduction workspace; all num_steps steps in one launch.
+struct GridArgs {
+    StepArgs base;
+    uint64_t first_step;
+    uint64_t num_steps;
+    double* trace;              // [num_steps]
+    double* bary;               // [3*num_steps] or nullptr
+    Partial* combined;          // [2] step partial by parity
+    unsigned long long* gen;    // generation word, zero at launch
+};
+
 struct EatArgs {
     SoA s;
     Scalars k;
@@ -195,6 +207,10 @@ cudaError_t launch_aos_to_soa(const void* aos, SoA s, double half_pond, uint64_t
                               int* mismatch, cudaStream_t st);
 cudaError_t launch_gather(const SoA& s, double half_pond, const uint64_t* idx, uint64_t cnt, void* aos,
                           cudaStream_t st);
+
+// Persistent cooperative-grid run; grid = SMs x occupancy of grid_kernel.
+int grid_kernel_blocks(int device);
+cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st);
 
 // Cluster kernel: returns cudaErrorNotSupported when n does not fit.
 int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta);

@@ -43,7 +43,8 @@ FISH_DTYPE = np.dtype(
     ]
 )
 
-STRATEGIES = {"auto": N.STRATEGY_AUTO, "stream": N.STRATEGY_STREAM, "persistent": N.STRATEGY_PERSISTENT}
+STRATEGIES = {"auto": N.STRATEGY_AUTO, "stream": N.STRATEGY_STREAM, "persistent": N.STRATEGY_PERSISTENT,
+              "grid": N.STRATEGY_GRID}
 
 
 @dataclass

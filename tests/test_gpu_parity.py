@@ -36,7 +36,7 @@ def rel_ok(got, want, rtol=BARY_RTOL):
     return np.all(np.abs(got - want) <= rtol * np.abs(want))
 
 
-STRATS = ["stream", "persistent"]
+STRATS = ["stream", "persistent", "grid"]
 
 
 def make(cfg, strategy="auto", **kw):

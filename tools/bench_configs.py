@@ -61,6 +61,7 @@ def main():
     ap.add_argument("--variants", action="store_true", help="also stream/persistent and alternate on/off")
     ap.add_argument("--bulk-ab", action="store_true", help="also the LDG step kernel (no bulk ring)")
     ap.add_argument("--pdl-ab", action="store_true", help="also without programmatic dependent launch")
+    ap.add_argument("--grid-ab", action="store_true", help="also the persistent cooperative-grid strategy")
     a = ap.parse_args()
     for name in a.only.split(","):
         n, t = CONFIGS[name]
@@ -75,6 +76,8 @@ def main():
             print(json.dumps(time_cfg(name, n, t, strategy, alt, a.reps, bulk)), flush=True)
         if a.pdl_ab and n > 32768:
             print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, True, pdl=False)), flush=True)
+        if a.grid_ab and n > 16384:
+            print(json.dumps(time_cfg(name, n, t, "grid", True, a.reps, True)), flush=True)
 
 
 if __name__ == "__main__":
