@@ -227,6 +227,27 @@ def load_profile_traffic(n: int):
     return None, None
 
 
+def issue_roofline(n: int, kernel_s: float, clocks: dict):
+    """The step kernel's second roofline: SM instruction issue (one warp
+    instruction per SMSP per cycle).  Instructions per fish from the committed
+    ncu capture (profiles/step_kernel_ncu.json), clock from the timed region."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "step_kernel_ncu.json")) as f:
+            p = json.load(f)
+        instr_per_fish = float(p["thread_instructions_per_fish"])
+    except Exception:
+        return None
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148
+    mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    peak = sms * 4 * mhz * 1e6  # warp instructions / s
+    achieved = instr_per_fish / 32.0 * n / kernel_s
+    return {"bound": "issue", "unit": "warp-instr/s", "instr_per_fish": instr_per_fish, "achieved": achieved,
+            "peak": peak, "frac": achieved / peak,
+            "note": "issue-active fraction the step kernel sustains; with HBM frac_moved ~0.8 both limits bind"}
+
+
 def run_ours(args, world, rank, local):
     import ctypes
 
@@ -350,6 +371,7 @@ def run_ours(args, world, rank, local):
                 "peak_source": peak_src,
                 "traffic_source": traffic_src,
             },
+            "issue_roofline": issue_roofline(n_local, kernel_s, clk.summary()),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
