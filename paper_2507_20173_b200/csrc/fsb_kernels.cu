@@ -459,6 +459,85 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
     }
 }
 
+#if FSB_LDG_PREFETCH
+// step_chunk with a per-thread cp.async (LDGSTS) prefetch ring: every thread
+// copies ITS OWN pair of the next FSB_LDG_PREFETCH-1 sub-tiles into shared
+// memory while it computes the current one, so the loads in flight cost no
+// registers and need no CTA-wide synchronisation (compact state, 1 pair/thread).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(gmem)
+                 : "memory");
+}
+
+__device__ __forceinline__ void step_chunk_prefetch(const StepArgs& a, const StepParams& P, bool eat,
+                                                    const SharedDivisor& M, uint64_t step, Partial& acc) {
+    constexpr int S = FSB_LDG_PREFETCH;
+    extern __shared__ __align__(16) unsigned char ldg_ring_raw[];  // S x 4 x kThreads double2
+    auto ring = reinterpret_cast<double2(*)[4][kThreads]>(ldg_ring_raw);
+    const uint64_t n = a.n;
+    const uint64_t npairs = n >> 1;
+    const bool rev = a.alternate && (step & 1ull);
+    constexpr uint64_t kAlign = 64;
+    const uint64_t nblk = (npairs + kAlign - 1) / kAlign;
+    const uint64_t lo = (nblk * blockIdx.x / gridDim.x) * kAlign;
+    uint64_t hi = (nblk * (blockIdx.x + 1) / gridDim.x) * kAlign;
+    if (hi > npairs) hi = npairs;
+    const uint64_t nsub = hi > lo ? (hi - lo + kThreads - 1) / kThreads : 0;
+    double2* X2 = reinterpret_cast<double2*>(a.s.x);
+    double2* Y2 = reinterpret_cast<double2*>(a.s.y);
+    double2* W2 = reinterpret_cast<double2*>(a.s.w);
+    double2* P2 = reinterpret_cast<double2*>(a.s.p);
+    const unsigned t = threadIdx.x;
+    auto pair_of = [&](uint64_t j) { return lo + (rev ? nsub - 1 - j : j) * kThreads + t; };
+    auto issue = [&](uint64_t j) {
+        const uint64_t q = pair_of(j);
+        if (q < hi) {
+            const int s = (int)(j % S);
+            cp_async16(&ring[s][0][t], X2 + q);
+            cp_async16(&ring[s][1][t], Y2 + q);
+            cp_async16(&ring[s][2][t], W2 + q);
+            cp_async16(&ring[s][3][t], P2 + q);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count aligned)
+    };
+    for (int j = 0; j < S - 1; ++j) issue(j);
+    const SoA2 src{X2, Y2, W2, P2, nullptr};
+    for (uint64_t j = 0; j < nsub; ++j) {
+        issue(j + S - 1);
+        asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // sub-tile j has landed
+        const uint64_t q = pair_of(j);
+        const int s = (int)(j % S);
+        double2 X[1], Y[1], W[1], Q[1];
+        const bool valid[1] = {q < hi};
+        const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
+        if (valid[0]) {
+            X[0] = ring[s][0][t];
+            Y[0] = ring[s][1][t];
+            W[0] = ring[s][2][t];
+            Q[0] = ring[s][3][t];
+        }
+        fused_pairs<false, 1>(X, Y, W, Q, X, valid, src, qs, gi, P, eat, M, step, acc);
+        if (valid[0]) {
+            X2[q] = X[0];
+            Y2[q] = Y[0];
+            W2[q] = W[0];
+            P2[q] = Q[0];
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if ((n & 1ull) && blockIdx.x == 0 && t == 0) {  // odd tail fish
+        const uint64_t i = n - 1;
+        double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];
+        fused_fish(x, y, w, p, objective(x, y, P.half_pond), eat, M, a.gfirst + i, step, P, acc);
+        a.s.x[i] = x;
+        a.s.y[i] = y;
+        a.s.w[i] = w;
+        a.s.p[i] = p;
+    }
+}
+#endif
+
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
     const StepParams P = params_of(a.k);
@@ -469,7 +548,11 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
     Partial acc = identity();
-    step_chunk<kExplicitCur>(a, P, eat, M, step, acc);
+#if FSB_LDG_PREFETCH
+    if (!kExplicitCur) step_chunk_prefetch(a, P, eat, M, step, acc);
+    else
+#endif
+        step_chunk<kExplicitCur>(a, P, eat, M, step, acc);
     grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 
@@ -649,6 +732,8 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
     __syncthreads();
 
     auto sub_base = [&](uint64_t j) { return lo + (rev ? nsub - 1 - j : j) * (uint64_t)kBulkTilePairs; };
+    // experiment-only FSB_MEM_WINDOW folds the addresses into an L2 window
+    auto mem_of = [&](uint64_t b) { return FSB_MEM_WINDOW ? lo + ((b - lo) % FSB_MEM_WINDOW) : b; };
     Partial acc = identity();
     if (t >= kBulkCompute) {
         // Producer warp, elected lane.  Sub-tile j lives in stage j % kBulkStages:
@@ -656,33 +741,38 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
         // into the stage (empty[s]), bulk-store the stage to HBM and, as soon as
         // the store has read the stage out, reuse it for sub-tile j + kBulkStages.
         if (t == kBulkCompute) {
+            auto mem = mem_of;
             auto load = [&](uint64_t j) {
                 const int s = (int)(j % kBulkStages);
                 const uint64_t base = sub_base(j);
                 const uint64_t cnt = (hi - base < (uint64_t)kBulkTilePairs) ? hi - base : (uint64_t)kBulkTilePairs;
                 const unsigned bytes = (unsigned)(cnt * sizeof(double2));
                 mbar_expect_tx(&full[s], 4 * bytes);
-                bulk_load(stage[s].x, X2 + base, bytes, &full[s]);
-                bulk_load(stage[s].y, Y2 + base, bytes, &full[s]);
-                bulk_load(stage[s].w, W2 + base, bytes, &full[s]);
-                bulk_load(stage[s].p, P2 + base, bytes, &full[s]);
+                bulk_load(stage[s].x, X2 + mem(base), bytes, &full[s]);
+                bulk_load(stage[s].y, Y2 + mem(base), bytes, &full[s]);
+                bulk_load(stage[s].w, W2 + mem(base), bytes, &full[s]);
+                bulk_load(stage[s].p, P2 + mem(base), bytes, &full[s]);
             };
             for (uint64_t j = 0; j < nsub && j < (uint64_t)kBulkStages; ++j) load(j);
             for (uint64_t j = 0; j < nsub; ++j) {
                 const int s = (int)(j % kBulkStages);
                 mbar_wait(&empty[s], (unsigned)((j / kBulkStages) & 1));
+#if FSB_BULK_STORE
                 const uint64_t base = sub_base(j);
                 const uint64_t cnt = (hi - base < (uint64_t)kBulkTilePairs) ? hi - base : (uint64_t)kBulkTilePairs;
                 const unsigned bytes = (unsigned)(cnt * sizeof(double2));
-                bulk_store(X2 + base, stage[s].x, bytes);
-                bulk_store(Y2 + base, stage[s].y, bytes);
-                bulk_store(W2 + base, stage[s].w, bytes);
-                bulk_store(P2 + base, stage[s].p, bytes);
+                bulk_store(X2 + mem(base), stage[s].x, bytes);
+                bulk_store(Y2 + mem(base), stage[s].y, bytes);
+                bulk_store(W2 + mem(base), stage[s].w, bytes);
+                bulk_store(P2 + mem(base), stage[s].p, bytes);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 if (j + kBulkStages < nsub) {
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     load(j + kBulkStages);
                 }
+#else
+                if (j + kBulkStages < nsub) load(j + kBulkStages);
+#endif
             }
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
         }
@@ -691,7 +781,14 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
             const int s = (int)(j % kBulkStages);
             const uint64_t base = sub_base(j);
             mbar_wait(&full[s], (unsigned)((j / kBulkStages) & 1));
+#if FSB_BULK_STORE
             const SoA2 src{stage[s].x, stage[s].y, stage[s].w, stage[s].p, nullptr};
+#else
+            // the stage is released as soon as it is in registers; a guard
+            // fallback re-reads the (not yet overwritten) state from HBM
+            const uint64_t mb = mem_of(base);
+            const SoA2 src{X2 + mb, Y2 + mb, W2 + mb, P2 + mb, nullptr};
+#endif
             double2 X[kBulkPairsPerThread], Y[kBulkPairsPerThread], W[kBulkPairsPerThread], Q[kBulkPairsPerThread];
             bool valid[kBulkPairsPerThread];
             uint64_t ks[kBulkPairsPerThread], gi[kBulkPairsPerThread];
@@ -708,21 +805,37 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
                     Q[u] = stage[s].p[k];
                 }
             }
+#if !FSB_BULK_STORE
+            __syncwarp();
+            if ((t & 31) == 0) mbar_arrive(&empty[s]);
+#endif
             fused_pairs<false, kBulkPairsPerThread>(X, Y, W, Q, X, valid, src, ks, gi, P, eat, M, step, acc);
 #pragma unroll
-            for (int u = 0; u < kBulkPairsPerThread; ++u) {  // new state back into the stage
+            for (int u = 0; u < kBulkPairsPerThread; ++u) {
                 const unsigned k = (unsigned)ks[u];
                 if (valid[u]) {
+#if FSB_BULK_STORE
+                    // new state back into the stage, bulk-stored by the producer
                     stage[s].x[k] = X[u];
                     stage[s].y[k] = Y[u];
                     stage[s].w[k] = W[u];
                     stage[s].p[k] = Q[u];
+#else
+                    // new state straight to HBM
+                    const uint64_t q = mem_of(base + k);
+                    X2[q] = X[u];
+                    Y2[q] = Y[u];
+                    W2[q] = W[u];
+                    P2[q] = Q[u];
+#endif
                 }
             }
+#if FSB_BULK_STORE
             // make the generic-proxy smem writes visible to the bulk-store (async) proxy
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&empty[s]);
+#endif
         }
         if ((n & 1ull) && blockIdx.x == 0 && t == 0) {  // odd tail fish
             const uint64_t i = n - 1;
@@ -1080,7 +1193,8 @@ int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
 #if FSB_SINGLE
             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_single, kThreads, 0);
 #else
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, 0);
+            : (cudaFuncSetAttribute(step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLdgRingBytes),
+               cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, kLdgRingBytes));
 #endif
     }
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
@@ -1122,7 +1236,7 @@ cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
 #if FSB_SINGLE
     return launch_maybe_pdl(step_kernel_single, grid, kThreads, 0, st, a, pdl);
 #else
-    return launch_maybe_pdl(step_kernel<false>, grid, kThreads, 0, st, a, pdl);
+    return launch_maybe_pdl(step_kernel<false>, grid, kThreads, kLdgRingBytes, st, a, pdl);
 #endif
 }
 

@@ -49,6 +49,12 @@ namespace fsb_dev {
 #ifndef FSB_BULK_MIN_BLOCKS
 #define FSB_BULK_MIN_BLOCKS 3
 #endif
+#ifndef FSB_LDG_PREFETCH
+#define FSB_LDG_PREFETCH 0  // >1: LDG step kernel prefetches through a per-thread cp.async ring
+#endif
+#ifndef FSB_BULK_STORE
+#define FSB_BULK_STORE 1  // 1: results bulk-stored from the stage; 0: STG from registers
+#endif
 #ifndef FSB_BULK_PAIRS
 #define FSB_BULK_PAIRS 1
 #endif
@@ -57,6 +63,7 @@ constexpr int kThreads = 256;     // threads per CTA of the streaming kernels
 constexpr int kPairsPerThread = FSB_PAIRS;  // double2 loads per array per thread per tile
 constexpr int kTilePairs = kThreads * kPairsPerThread;
 constexpr int kTileFish = 2 * kTilePairs;
+constexpr int kLdgRingBytes = FSB_LDG_PREFETCH * 4 * kThreads * 16;  // dynamic smem of step_kernel<false>
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,
 // plus one producer warp; a kBulkStages-deep ring of sub-tiles in smem.

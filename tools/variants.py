@@ -28,6 +28,16 @@ VARIANTS = {
     "b1s4m3": ["-DFSB_BULK_PAIRS=1", "-DFSB_BULK_STAGES=4", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b4s2m1": ["-DFSB_BULK_PAIRS=4", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=1"],
+    # LDG kernel with a per-thread cp.async prefetch ring of S sub-tiles
+    "pf2": ["-DFSB_LDG_PREFETCH=2"],
+    "pf3": ["-DFSB_LDG_PREFETCH=3"],
+    "pf4": ["-DFSB_LDG_PREFETCH=4", "-DFSB_MIN_BLOCKS=3"],
+    "l2_pf3": ["-DFSB_LDG_PREFETCH=3", "-DFSB_MEM_WINDOW=512"],
+    # bulk ring with direct STG stores (stage released right after the LDS)
+    "stg": ["-DFSB_BULK_STORE=0"],
+    "stg_b2s3m2": ["-DFSB_BULK_STORE=0", "-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=3", "-DFSB_BULK_MIN_BLOCKS=2"],
+    "l2_stg": ["-DFSB_BULK_STORE=0", "-DFSB_MEM_WINDOW=512"],
+    "l2_bulk": ["-DFSB_MEM_WINDOW=512"],
     # RNG high-word shifts on the fma pipe (IMAD.HI) instead of the alu pipe
     "imadsh": ["-DFSB_IMAD_SHIFTS=1"],
     "imadsh_p2b3": ["-DFSB_IMAD_SHIFTS=1", "-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=3"],
