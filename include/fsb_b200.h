@@ -83,6 +83,8 @@ enum fsb_strategy {
 #define FSB_FLAG_NO_PDL 0x10u      /* no Programmatic Dependent Launch between graph step kernels */
 #define FSB_FLAG_PEER_EXCHANGE 0x20u /* per-step exchange by NVLink peer stores from the step kernel
                                         itself (CUDA IPC windows) instead of an NCCL allgather */
+#define FSB_FLAG_CHECKED 0x40u     /* always evaluate the fp64 fast-path operand guards (default: elided
+                                      while config and state are provably in range; results identical) */
 
 typedef struct fsb_engine_options {
     int device;                  /* CUDA device ordinal of this shard */

@@ -30,6 +30,7 @@ FLAG_NO_BULK = 0x4
 FLAG_FORCE_BULK = 0x8
 FLAG_NO_PDL = 0x10
 FLAG_PEER_EXCHANGE = 0x20
+FLAG_CHECKED = 0x40
 
 
 class fsb_sim_config(ctypes.Structure):

@@ -281,12 +281,13 @@ __device__ __forceinline__ void fused_fish(double& x, double& y, double& w, doub
 // The same fish update on the guarded fast paths: returns the new objective
 // and ANDs the operand guards into ok (no accumulation: the caller folds the
 // fish into its partial once the result is final).
+template <bool kSane>
 __device__ __forceinline__ double fused_fish_guarded(double& x, double& y, double& w, double& p,
                                                      double cur, bool eat, const SharedDivisor& M,
                                                      uint64_t gi, uint64_t step, const StepParams& P,
                                                      bool& ok) {
-    if (eat) w = eat_weight_guarded(w, p, cur, M, P.w_max, ok);
-    const double cn = swim_guarded(x, y, w, fold_in(P.seed, gi), step, P, ok);
+    if (eat) w = eat_weight_guarded<kSane>(w, p, cur, M, P.w_max, ok);
+    const double cn = swim_guarded<kSane>(x, y, w, fold_in(P.seed, gi), step, P, ok);
     p = cur;
     return cn;
 }
@@ -319,8 +320,10 @@ struct SoA2 {
 // re-read from src at index k[u].  All 2U fish run their guarded fast paths
 // first (independent chains the scheduler interleaves), then ONE warp vote:
 // a pair whose guard failed is recomputed with the exact intrinsics.  Only
-// then are the fish folded into the thread partial.
-template <bool kExplicitCur, int U>
+// then are the fish folded into the thread partial.  kSane: the state is in
+// range (fsb_math.cuh "In-range mode"); the eat divisor -- the global max,
+// which other ranks' states feed -- is range-checked here, once per call.
+template <bool kExplicitCur, int U, bool kSane>
 __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], double2 (&W)[U],
                                             double2 (&Q)[U], const double2 (&C)[U], const bool (&valid)[U],
                                             const SoA2& src, const uint64_t (&k)[U], const uint64_t (&gi)[U],
@@ -329,14 +332,20 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
     bool ok[U];
     double n0[U], n1[U];
     bool all_ok = true;
+    // M.b in [2^-506, 2^502] (positive: as an integer range on its bits)
+    const uint64_t mb = static_cast<uint64_t>(__double_as_longlong(M.b));
+    const bool ok0 = !kSane || !eat || (mb - 0x2050000000000000ull <= 0x3F00000000000000ull);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        ok[u] = true;
+        ok[u] = ok0;
         if (valid[u]) {
-            const double c0 = kExplicitCur ? C[u].x : objective_guarded(X[u].x, Y[u].x, P.half_pond, ok[u]);
-            const double c1 = kExplicitCur ? C[u].y : objective_guarded(X[u].y, Y[u].y, P.half_pond, ok[u]);
-            n0[u] = fused_fish_guarded(X[u].x, Y[u].x, W[u].x, Q[u].x, c0, eat, M, gi[u], step, P, ok[u]);
-            n1[u] = fused_fish_guarded(X[u].y, Y[u].y, W[u].y, Q[u].y, c1, eat, M, gi[u] + 1, step, P, ok[u]);
+            const double c0 =
+                kExplicitCur ? C[u].x : objective_guarded<kSane>(X[u].x, Y[u].x, P.half_pond, ok[u]);
+            const double c1 =
+                kExplicitCur ? C[u].y : objective_guarded<kSane>(X[u].y, Y[u].y, P.half_pond, ok[u]);
+            n0[u] = fused_fish_guarded<kSane>(X[u].x, Y[u].x, W[u].x, Q[u].x, c0, eat, M, gi[u], step, P, ok[u]);
+            n1[u] = fused_fish_guarded<kSane>(X[u].y, Y[u].y, W[u].y, Q[u].y, c1, eat, M, gi[u] + 1, step, P,
+                                              ok[u]);
             all_ok &= ok[u];
         }
     }
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(kThreads) init_kernel(const InitArgs a) {
 
 // This CTA's share of one fused step (LDG path): its balanced chunk of pairs,
 // plus the odd tail fish on CTA 0.  Folds every fish into acc.
-template <bool kExplicitCur>
+template <bool kExplicitCur, bool kSane>
 __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& P, bool eat,
                                            const SharedDivisor& M, uint64_t step, Partial& acc) {
     const uint64_t n = a.n;
@@ -435,7 +444,7 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
             }
         }
         const SoA2 src{X2, Y2, W2, P2, C2};
-        fused_pairs<kExplicitCur, kPairsPerThread>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
+        fused_pairs<kExplicitCur, kPairsPerThread, kSane>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
 #pragma unroll
         for (int u = 0; u < kPairsPerThread; ++u) {
             const uint64_t q = qs[u];
@@ -517,7 +526,7 @@ __device__ __forceinline__ void step_chunk_prefetch(const StepArgs& a, const Ste
             W[0] = ring[s][2][t];
             Q[0] = ring[s][3][t];
         }
-        fused_pairs<false, 1>(X, Y, W, Q, X, valid, src, qs, gi, P, eat, M, step, acc);
+        fused_pairs<false, 1, false>(X, Y, W, Q, X, valid, src, qs, gi, P, eat, M, step, acc);
         if (valid[0]) {
             X2[q] = X[0];
             Y2[q] = Y[0];
@@ -538,7 +547,7 @@ __device__ __forceinline__ void step_chunk_prefetch(const StepArgs& a, const Ste
 }
 #endif
 
-template <bool kExplicitCur>
+template <bool kExplicitCur, bool kSane>
 __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
     const StepParams P = params_of(a.k);
     pdl_wait_and_release();
@@ -552,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
     if (!kExplicitCur) step_chunk_prefetch(a, P, eat, M, step, acc);
     else
 #endif
-        step_chunk<kExplicitCur>(a, P, eat, M, step, acc);
+        step_chunk<kExplicitCur, kSane>(a, P, eat, M, step, acc);
     grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 
@@ -564,6 +573,7 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
 // the step's partial and trace entry, and opens the next generation; the
 // others sleep on the generation word.  Co-residency of all CTAs is
 // guaranteed by the cooperative launch.
+template <bool kSane>
 __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) grid_kernel(const GridArgs g) {
     const StepArgs& a = g.base;
     const StepParams P = params_of(a.k);
@@ -576,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) grid_kernel(const Gr
         const bool eat = prev.best > 0.0;
         const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
         Partial acc = identity();
-        step_chunk<false>(a, P, eat, M, step, acc);
+        step_chunk<false, kSane>(a, P, eat, M, step, acc);
         const Partial blk = block_reduce(acc, scratch);
         if (threadIdx.x == 0) {
             store_partial(&a.ws.block_part[blockIdx.x], blk);
@@ -692,6 +702,7 @@ struct BulkStage {
 
 // Warps 0..7 compute (kBulkPairsPerThread pairs each per sub-tile); warp 8 is
 // the producer whose elected lane keeps the ring full.
+template <bool kSane>
 __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel_bulk(const StepArgs a) {
     extern __shared__ __align__(128) unsigned char bulk_smem[];
     BulkStage* stage = reinterpret_cast<BulkStage*>(bulk_smem);
@@ -809,7 +820,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&empty[s]);
 #endif
-            fused_pairs<false, kBulkPairsPerThread>(X, Y, W, Q, X, valid, src, ks, gi, P, eat, M, step, acc);
+            fused_pairs<false, kBulkPairsPerThread, kSane>(X, Y, W, Q, X, valid, src, ks, gi, P, eat, M, step, acc);
 #pragma unroll
             for (int u = 0; u < kBulkPairsPerThread; ++u) {
                 const unsigned k = (unsigned)ks[u];
@@ -880,7 +891,7 @@ __global__ void __launch_bounds__(kThreads, FSB_SINGLE_MIN_BLOCKS) step_kernel_s
             w = a.s.w[i];
             p = a.s.p[i];
             const double c = objective_guarded(x, y, P.half_pond, ok);
-            cn = fused_fish_guarded(x, y, w, p, c, eat, M, a.gfirst + i, step, P, ok);
+            cn = fused_fish_guarded<false>(x, y, w, p, c, eat, M, a.gfirst + i, step, P, ok);
         }
         if (__any_sync(0xffffffffu, !ok)) {
             if (!ok) {
@@ -979,10 +990,18 @@ __global__ void soa_to_aos_kernel(const SoA s, double half, uint64_t lo, uint64_
     }
 }
 
+// {+0} U [2^-454, 2^501]: the objective values an in-range state can hold.
+__device__ __forceinline__ bool objective_in_range(double v) {
+    return __double_as_longlong(v) == 0 || (v >= 0x1p-454 && v <= 0x1p501);
+}
+
+// Upload: AoS -> SoA.  mismatch |= 1 if some current_objective differs from
+// objective(x, y) (the state then carries an explicit c[]), |= 2 if some fish
+// is outside the in-range mode's preconditions.
 __global__ void aos_to_soa_kernel(const FishAoS* in, SoA s, double half, uint64_t lo, uint64_t cnt,
                                   int* mismatch) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    bool bad = false;
+    bool bad = false, out = false;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += stride) {
         const uint64_t i = lo + k;
         const FishAoS f = in[k];
@@ -994,8 +1013,13 @@ __global__ void aos_to_soa_kernel(const FishAoS* in, SoA s, double half, uint64_
         // bitwise comparison: is current_objective the objective of (x, y)?
         const double o = objective(f.x, f.y, half);
         bad |= (__double_as_longlong(o) != __double_as_longlong(f.c));
+        // in-range mode preconditions (fsb_math.cuh "In-range mode")
+        const double pond = 2.0 * half;
+        out |= !(f.x >= 0.0 && f.x <= pond && f.y >= 0.0 && f.y <= pond) || f.w > 0x1p501 ||
+               !objective_in_range(f.p) || !objective_in_range(f.c);
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(mismatch, 1);
+    const int flags = (__syncthreads_or(bad) ? 1 : 0) | (__syncthreads_or(out) ? 2 : 0);
+    if (flags && threadIdx.x == 0) atomicOr(mismatch, flags);
 }
 
 // ---------------------------------------------------------------------------
@@ -1185,16 +1209,22 @@ int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
     int per_sm = 0;
     cudaError_t e;
     if (bulk && !explicit_cur) {
-        cudaFuncSetAttribute(step_kernel_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmemBytes);
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_bulk, kBulkThreads, kBulkSmemBytes);
+        cudaFuncSetAttribute(step_kernel_bulk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmemBytes);
+        cudaFuncSetAttribute(step_kernel_bulk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmemBytes);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_bulk<false>, kBulkThreads,
+                                                          kBulkSmemBytes);
     } else {
         e = explicit_cur
-            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true>, kThreads, 0)
+            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true, false>, kThreads, 0)
 #if FSB_SINGLE
             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_single, kThreads, 0);
 #else
-            : (cudaFuncSetAttribute(step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kLdgRingBytes),
-               cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false>, kThreads, kLdgRingBytes));
+            : (cudaFuncSetAttribute(step_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kLdgRingBytes),
+               cudaFuncSetAttribute(step_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kLdgRingBytes),
+               cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false, false>, kThreads,
+                                                             kLdgRingBytes));
 #endif
     }
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
@@ -1231,12 +1261,18 @@ cudaError_t launch_maybe_pdl(void (*kern)(Args), int grid, int block, size_t sme
 
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
     const bool pdl = a.pdl != 0;
-    if (a.s.c) return launch_maybe_pdl(step_kernel<true>, grid, kThreads, 0, st, a, pdl);
-    if (a.bulk) return launch_maybe_pdl(step_kernel_bulk, grid, kBulkThreads, kBulkSmemBytes, st, a, pdl);
+    const bool sane = a.sane != 0;
+    if (a.s.c)
+        return launch_maybe_pdl(sane ? step_kernel<true, true> : step_kernel<true, false>, grid, kThreads, 0, st,
+                                a, pdl);
+    if (a.bulk)
+        return launch_maybe_pdl(sane ? step_kernel_bulk<true> : step_kernel_bulk<false>, grid, kBulkThreads,
+                                kBulkSmemBytes, st, a, pdl);
 #if FSB_SINGLE
     return launch_maybe_pdl(step_kernel_single, grid, kThreads, 0, st, a, pdl);
 #else
-    return launch_maybe_pdl(step_kernel<false>, grid, kThreads, kLdgRingBytes, st, a, pdl);
+    return launch_maybe_pdl(sane ? step_kernel<false, true> : step_kernel<false, false>, grid, kThreads,
+                            kLdgRingBytes, st, a, pdl);
 #endif
 }
 
@@ -1247,18 +1283,23 @@ cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st) {
 }
 
 int grid_kernel_blocks(int device) {
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_kernel, kThreads, 0) != cudaSuccess ||
-        per_sm < 1) {
+    // co-residency of every CTA: the smaller occupancy of the two instantiations
+    int per_sm = 0, per_sm_sane = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_kernel<false>, kThreads, 0) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sane, grid_kernel<true>, kThreads, 0) !=
+            cudaSuccess) {
         cudaGetLastError();
-        per_sm = 1;
+        per_sm = per_sm_sane = 1;
     }
-    return num_sms(device) * per_sm;
+    if (per_sm_sane < per_sm) per_sm = per_sm_sane;
+    return num_sms(device) * (per_sm < 1 ? 1 : per_sm);
 }
 
 cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st) {
     void* args[] = {const_cast<GridArgs*>(&g)};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(grid_kernel), dim3(grid), dim3(kThreads), args,
+    const void* kern = g.base.sane ? reinterpret_cast<const void*>(grid_kernel<true>)
+                                   : reinterpret_cast<const void*>(grid_kernel<false>);
+    return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args,
                                        0, st);
 }
 

@@ -146,6 +146,7 @@ struct StepArgs {
     int bulk;             // stream through shared memory with cp.async.bulk (compact state)
     int pdl;              // launched as a programmatic dependent of the previous step
     PeerXchg px;          // peer exchange instead of part_in/part_out (px.peers != nullptr)
+    int sane;             // state and config in range: guards elided (fsb_math.cuh "In-range mode")
 };
 
 // Persistent cooperative-grid run (FSB_STRATEGY_GRID): `base` supplies the

@@ -135,13 +135,14 @@ class Engine:
     def __init__(self, cfg: SimConfig, device: int = 0, rank: int = 0, world_size: int = 1,
                  nccl_unique_id: Optional[bytes] = None, strategy: str = "auto",
                  alternate: bool = True, force_nccl: bool = False, bulk=True, pdl: bool = True,
-                 peer: bool = False):
+                 peer: bool = False, checked: bool = False):
         self.cfg = cfg
         L = N.lib()
         self._uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
         flags = ((0 if alternate else N.FLAG_NO_ALTERNATE) | (N.FLAG_FORCE_NCCL if force_nccl else 0)
                  | (0 if bulk else N.FLAG_NO_BULK) | (N.FLAG_FORCE_BULK if bulk == "force" else 0)
-                 | (0 if pdl else N.FLAG_NO_PDL) | (N.FLAG_PEER_EXCHANGE if peer else 0))
+                 | (0 if pdl else N.FLAG_NO_PDL) | (N.FLAG_PEER_EXCHANGE if peer else 0)
+                 | (N.FLAG_CHECKED if checked else 0))
         opts = N.fsb_engine_options(device, rank, world_size,
                                     ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
                                     STRATEGIES[strategy], flags)

@@ -234,6 +234,83 @@ def test_upload_inconsistent_then_run(orc, strategy):
         assert eng.download().tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("strategy", ["stream", "grid"])
+@pytest.mark.parametrize("bulk", [False, "force"])
+@pytest.mark.parametrize("n,t", [(4097, 9), (300_001, 5)])
+def test_in_range_mode_equals_checked(orc, strategy, bulk, n, t):
+    """The step kernels with the fp64 operand guards elided (in-range mode, the
+    default for an init'd school) and evaluated (FSB_FLAG_CHECKED) agree with
+    the oracle bit for bit."""
+    cfg = fsb.baseline_config(n, t)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    for checked in (False, True):
+        with make(cfg, strategy, bulk=bulk, checked=checked) as eng:
+            trace, _, _ = eng.simulate(barycentre=False)
+            assert trace.tobytes() == want_trace.tobytes(), checked
+            assert eng.download().tobytes() == want_fish.tobytes(), checked
+
+
+def _hostile(kind, n, rng):
+    fish = np.zeros(n, dtype=oracle.FISH_DTYPE)
+    fish["x"] = rng.uniform(0, 200, n)
+    fish["y"] = rng.uniform(0, 200, n)
+    fish["weight"] = rng.uniform(1, 20, n)
+    o = np.sqrt((fish["x"] - 100) ** 2 + (fish["y"] - 100) ** 2)
+    fish["prev_objective"] = o
+    fish["current_objective"] = o
+    k = slice(0, n, 7)
+    if kind == "denormal_prev":
+        fish["prev_objective"][k] = 5e-310
+    elif kind == "huge_weight":
+        fish["weight"][k] = 1e300
+    elif kind == "outside_pond":
+        fish["x"][k] = -3.0
+        fish["y"][1::7] = 1e6
+    elif kind == "centre_and_ties":
+        fish["x"][k] = 100.0
+        fish["y"][k] = 100.0
+        fish["prev_objective"][k] = 0.0
+        fish["current_objective"][k] = 0.0
+        fish["prev_objective"][1::7] = fish["current_objective"][1::7]
+    elif kind == "negative_zero":
+        fish["prev_objective"][k] = -0.0
+    return fish
+
+
+@pytest.mark.parametrize("strategy", ["stream", "persistent"])
+@pytest.mark.parametrize("kind", ["denormal_prev", "huge_weight", "outside_pond", "centre_and_ties",
+                                  "negative_zero"])
+def test_upload_out_of_range_state(orc, strategy, kind):
+    """States outside the in-range mode's bounds (fsb_math.cuh) take the guarded
+    kernels and still match the oracle; in-range edge values (fish at the pond
+    centre, prev == cur) are exact in either mode."""
+    n = 5003
+    fish = _hostile(kind, n, np.random.default_rng(23))
+    cfg = fsb.SimConfig(num_fish=n, num_steps=5, seed=29)
+    oc = ocfg(cfg)
+    for checked in (False, True):
+        with make(cfg, strategy, checked=checked) as eng:
+            eng.upload(fish)
+            want = fish.copy()
+            trace, _, _ = eng.run(0, 5)
+            assert trace.tobytes() == orc.run(oc, want, 0, 5).tobytes(), (kind, checked)
+            assert eng.download().tobytes() == want.tobytes(), (kind, checked)
+
+
+@pytest.mark.parametrize("over", [dict(pond_size=1e-130), dict(pond_size=1e160), dict(step_base=1e-125),
+                                  dict(step_base=1e200), dict(weight_scale=1e160)])
+def test_config_outside_in_range_bounds(orc, over):
+    """Configurations outside the in-range bounds run the guarded kernels."""
+    kw = dict(num_fish=20_001, num_steps=6, seed=31)
+    kw.update(over)
+    cfg = fsb.SimConfig(**kw)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "stream") as eng:
+        trace, _, _ = eng.simulate(barycentre=False)
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == want_fish.tobytes()
+
+
 def test_long_stream_run_is_chunked(orc):
     """A run longer than one graph (1024 steps) goes through several graphs."""
     cfg = fsb.baseline_config(20_000, 2500)

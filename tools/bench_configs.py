@@ -35,9 +35,9 @@ def peak():
         return 6650.0
 
 
-def time_cfg(name, n, t, strategy, alternate, reps, bulk=True, pdl=True):
+def time_cfg(name, n, t, strategy, alternate, reps, bulk=True, pdl=True, checked=False):
     cfg = fsb.baseline_config(n, t)
-    with fsb.Engine(cfg, strategy=strategy, alternate=alternate, bulk=bulk, pdl=pdl) as eng:
+    with fsb.Engine(cfg, strategy=strategy, alternate=alternate, bulk=bulk, pdl=pdl, checked=checked) as eng:
         eng.init()
         eng.run(0, t)  # warm-up of the same shape (graph instantiation)
         secs = []
@@ -49,7 +49,7 @@ def time_cfg(name, n, t, strategy, alternate, reps, bulk=True, pdl=True):
         ck = None
     rate = n * t / s
     return {"config": name, "fish": n, "steps": t, "strategy": strategy, "alternate": alternate, "bulk": bulk,
-            "pdl": pdl,
+            "pdl": pdl, "checked": checked,
             "seconds": s, "fish_updates_per_s": rate, "us_per_step": 1e6 * s / t,
             "hbm_frac_80B": rate * 80 / 1e9 / peak(), "hbm_frac_64B": rate * 64 / 1e9 / peak()}
 
@@ -62,6 +62,7 @@ def main():
     ap.add_argument("--bulk-ab", action="store_true", help="also the LDG step kernel (no bulk ring)")
     ap.add_argument("--pdl-ab", action="store_true", help="also without programmatic dependent launch")
     ap.add_argument("--grid-ab", action="store_true", help="also the persistent cooperative-grid strategy")
+    ap.add_argument("--checked-ab", action="store_true", help="also with the fp64 guards always evaluated")
     a = ap.parse_args()
     for name in a.only.split(","):
         n, t = CONFIGS[name]
@@ -76,6 +77,9 @@ def main():
             print(json.dumps(time_cfg(name, n, t, strategy, alt, a.reps, bulk)), flush=True)
         if a.pdl_ab and n > 32768:
             print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, True, pdl=False)), flush=True)
+        if a.checked_ab and n > 32768:
+            for bulk in (True, False):
+                print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, bulk, checked=True)), flush=True)
         if a.grid_ab and n > 16384:
             print(json.dumps(time_cfg(name, n, t, "grid", True, a.reps, True)), flush=True)
 
