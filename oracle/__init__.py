@@ -99,6 +99,7 @@ class Oracle:
             "oracle_checksum_update": (u64, [u64, vp, u64]),
             "oracle_barycentre_sums": (None, [vp, u64, vp]),
             "oracle_replay_fish": (None, [cp, u64, vp, u64, vp]),
+            "oracle_replay_many": (None, [cp, vp, u64, vp, u64, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -150,11 +151,9 @@ class Oracle:
     def replay(self, cfg, indices, trace):
         """Replay the given global fish indices alone with a run's max_diff trace."""
         trace = np.ascontiguousarray(trace, dtype=np.float64)
-        out = np.zeros(len(indices), dtype=FISH_DTYPE)
-        one = np.zeros(1, dtype=FISH_DTYPE)
-        for k, i in enumerate(indices):
-            self.L.oracle_replay_fish(ctypes.byref(cfg), int(i), _ptr(trace), len(trace), _ptr(one))
-            out[k] = one[0]
+        idx = np.ascontiguousarray(indices, dtype=np.uint64)
+        out = np.zeros(len(idx), dtype=FISH_DTYPE)
+        self.L.oracle_replay_many(ctypes.byref(cfg), _ptr(idx), len(idx), _ptr(trace), len(trace), _ptr(out))
         return out
 
 

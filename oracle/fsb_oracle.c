@@ -146,6 +146,11 @@ void oracle_replay_fish(const oracle_config* cfg, uint64_t i, const double* trac
     }
 }
 
+void oracle_replay_many(const oracle_config* cfg, const uint64_t* idx, uint64_t count, const double* trace,
+                        uint64_t num_steps, oracle_fish* out) {
+    for (uint64_t k = 0; k < count; ++k) oracle_replay_fish(cfg, idx[k], trace, num_steps, out + k);
+}
+
 /* sim.hpp:133-147 */
 void oracle_simulate(const oracle_config* cfg, oracle_fish* fish_out, double* trace) {
     oracle_init(cfg, 0, cfg->num_fish, fish_out);

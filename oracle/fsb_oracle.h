@@ -79,6 +79,10 @@ void oracle_run(const oracle_config* cfg, oracle_fish* fish, uint64_t n, uint64_
 void oracle_replay_fish(const oracle_config* cfg, uint64_t i, const double* trace, uint64_t num_steps,
                         oracle_fish* out);
 
+/* The same for count fish given by global index (out[k] = fish idx[k]). */
+void oracle_replay_many(const oracle_config* cfg, const uint64_t* idx, uint64_t count, const double* trace,
+                        uint64_t num_steps, oracle_fish* out);
+
 /* checksum (sim.hpp:154-176): FNV-1a 64 over the LE bytes of every field. */
 uint64_t oracle_checksum(const oracle_fish* fish, uint64_t n);
 /* Streamed form: continue hash h over more fish (h0 = 0xcbf29ce484222325). */

@@ -505,7 +505,7 @@ def test_gather_matches_download(orc):
 
 def test_c3_billion_fish(golden_baseline, orc):
     """C3 (1e9 fish x 20 steps, 32 GB of state): the max_diff trace against the
-    reference's, 20,000 sampled fish replayed on the CPU from their initial state
+    reference's, 1,000,000 sampled fish replayed on the CPU from their initial state
     with the GPU trace, the final checksum streamed over all 40 GB
     of Fish bytes, and the barycentre."""
     cfg = fsb.baseline_config(10**9, 20)
@@ -515,7 +515,7 @@ def test_c3_billion_fish(golden_baseline, orc):
         if g:
             assert [bits(v) for v in trace] == g["trace_hex"]
         rng = np.random.default_rng(3)
-        idx = np.unique(np.concatenate([rng.integers(0, 10**9, 20_000), [0, 1, 10**9 - 2, 10**9 - 1]]))
+        idx = np.unique(np.concatenate([rng.integers(0, 10**9, 1_000_000), [0, 1, 10**9 - 2, 10**9 - 1]]))
         got = eng.gather(idx.astype(np.uint64))
         want = orc.replay(ocfg(cfg), idx, trace)
         assert got.tobytes() == want.tobytes()
