@@ -733,6 +733,10 @@ int fsb_engine_upload(fsb_engine* e, const fsb_fish* fish, uint64_t count) {
     if (count && !fish) return fail(FSB_ERR_INVALID_ARGUMENT, "null fish");
     if (!e->c_buf) CU(cudaMalloc(&e->c_buf, (e->count ? e->count : 1) * sizeof(double)));
     TRY(ensure_staging(e));
+    // until the upload completes the state is unknown: checked kernels, explicit cur
+    e->state_sane = false;
+    e->cur_explicit = true;
+    e->max_valid = false;
     fsb_dev::SoA s = e->s;
     s.c = e->c_buf;
     CU(cudaMemsetAsync(e->d_mismatch, 0, sizeof(int), e->stream));
@@ -961,7 +965,15 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
         for (uint64_t k = 0; k < num_steps; ++k) kernel_ms[k] = 0.0;
         return FSB_OK;
     }
-    std::vector<cudaEvent_t> ev(num_steps + 1);
+    struct Events {  // destroyed on every return path
+        std::vector<cudaEvent_t> v;
+        ~Events() {
+            for (cudaEvent_t x : v)
+                if (x) cudaEventDestroy(x);
+        }
+    } events;
+    events.v.assign(num_steps + 1, nullptr);
+    std::vector<cudaEvent_t>& ev = events.v;
     for (auto& v : ev) CU(cudaEventCreate(&v));
     CU(cudaEventRecord(ev[0], e->stream));
     const uint64_t x0 = e->xseq;
@@ -996,7 +1008,6 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
         CU(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
         kernel_ms[k] = ms;
     }
-    for (auto& v : ev) cudaEventDestroy(v);
     return FSB_OK;
 }
 
