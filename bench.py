@@ -268,7 +268,7 @@ def run_ours(args, world, rank, local):
     elif args.force_nccl:
         uid = fsb.nccl_unique_id()
     eng = fsb.Engine(cfg, device=local, rank=rank, world_size=world, nccl_unique_id=uid,
-                     strategy=args.strategy, alternate=not args.no_alternate, bulk=not args.no_bulk,
+                     strategy=args.strategy, alternate=not args.no_alternate, bulk=args.bulk,
                      force_nccl=args.force_nccl, peer=args.peer)
     if args.peer and world > 1:
         import torch.distributed as dist
@@ -391,8 +391,8 @@ def main():
     ap.add_argument("--strategy", default="auto", choices=["auto", "stream", "persistent"])
     ap.add_argument("--no-alternate", action="store_true",
                     help="fixed tile order (default reverses odd steps to reuse L2 across steps)")
-    ap.add_argument("--no-bulk", action="store_true",
-                    help="LDG step kernel instead of the cp.async.bulk shared-memory ring")
+    ap.add_argument("--bulk", action="store_true",
+                    help="cp.async.bulk shared-memory ring step kernel instead of the LDG one (A/B)")
     ap.add_argument("--force-nccl", action="store_true",
                     help="exercise the NCCL exchange path even on one rank (testing)")
     ap.add_argument("--peer", action="store_true",

@@ -78,8 +78,9 @@ enum fsb_strategy {
 /* Engine flags. */
 #define FSB_FLAG_NO_ALTERNATE 0x1u /* keep tile order fixed (default reverses odd steps for L2 reuse) */
 #define FSB_FLAG_FORCE_NCCL 0x2u   /* use the NCCL exchange even when world_size == 1 (testing) */
-#define FSB_FLAG_NO_BULK 0x4u      /* step kernel loads with LDG instead of the cp.async.bulk smem ring */
-#define FSB_FLAG_FORCE_BULK 0x8u   /* bulk ring even for schools too small to amortise it (testing) */
+#define FSB_FLAG_NO_BULK 0x4u      /* LDG step kernel (the default; overrides FSB_FLAG_FORCE_BULK) */
+#define FSB_FLAG_FORCE_BULK 0x8u   /* step kernel streams through the cp.async.bulk shared-memory ring
+                                      (measured 2-3% slower than LDG in in-range mode; A/B) */
 #define FSB_FLAG_NO_PDL 0x10u      /* no Programmatic Dependent Launch between graph step kernels */
 #define FSB_FLAG_PEER_EXCHANGE 0x20u /* per-step exchange by NVLink peer stores from the step kernel
                                         itself (CUDA IPC windows) instead of an NCCL allgather */
@@ -179,6 +180,14 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
 
 /* Kernel launch count of the last fsb_engine_run (for bench accounting). */
 int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches);
+
+/* Configuration sweeps (the GPU analogue of the reference's thread-count
+ * experiments, bench.hpp:79-148): set the CTA count of the compact-state step
+ * and eat kernels (ctas = 0 restores the automatic SMs x occupancy grid).  Each
+ * CTA owns one balanced contiguous chunk, so results do not depend on it.
+ * fsb_engine_grid reports the grid in use and the threads per CTA. */
+int fsb_engine_set_grid(fsb_engine* e, int ctas);
+int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta);
 
 /* Peer exchange (FSB_FLAG_PEER_EXCHANGE, one process per GPU): each rank
  * exports its 64-byte CUDA IPC handle of its exchange window, the caller

@@ -29,10 +29,20 @@ def _config(a) -> sim.SimConfig:
     return sim.SimConfig(num_fish=a.fish, num_steps=a.steps, seed=a.seed)
 
 
+def _sms(device: int) -> int:
+    try:
+        import torch
+
+        return torch.cuda.get_device_properties(device).multi_processor_count
+    except Exception:
+        return 148
+
+
 def _record(experiment, strategy, cfg, eng, t, rep, threads=1) -> records.BenchRecord:
+    # threads = GPU threads of the step kernel's grid; chunk = fish per thread
     return records.BenchRecord(experiment=experiment, threads=threads,
                                schedule="cluster" if strategy == "persistent" else "graph",
-                               chunk=cfg.num_fish // threads, construct="gpu", rep=rep, fish=cfg.num_fish,
+                               chunk=max(1, cfg.num_fish // threads), construct="gpu", rep=rep, fish=cfg.num_fish,
                                steps=cfg.num_steps, seconds_total=t.seconds_total, seconds_eat=t.seconds_eat,
                                checksum=eng.checksum())
 
@@ -71,16 +81,23 @@ def cmd_gpuexp(a) -> int:
     cfg = _config(a)
     cfg.validate()
     recs = []
-    plans = [("gpu-stream", "stream", True), ("gpu-stream-ldg", "stream", False)]
+    # (experiment, strategy, step kernel, CTAs per SM or None = automatic grid)
+    plans = [("gpu-stream", "stream", False, None), ("gpu-stream-bulk", "stream", True, None)]
     if cfg.num_fish <= 16384:
-        plans.append(("gpu-persistent", "persistent", True))
-    for name, strategy, bulk in plans:
+        plans.append(("gpu-persistent", "persistent", False, None))
+    # Exp 1 analogue (thread count): the CTA count of the step kernel, 1..8 per SM
+    plans += [("gpu-grid", "stream", False, k) for k in (1, 2, 4, 8)]
+    for name, strategy, bulk, per_sm in plans:
         try:
             with sim.Engine(cfg, device=a.device, strategy=strategy, bulk=bulk) as eng:
+                if per_sm:
+                    eng.set_grid(per_sm * _sms(a.device))
+                ctas, tpc = eng.grid()
+                threads = 1 if strategy == "persistent" else ctas * tpc
                 for r in range(a.warmup + a.reps):
                     _, _, t = eng.simulate(barycentre=False)
                     if r >= a.warmup:
-                        recs.append(_record(name, strategy, cfg, eng, t, r - a.warmup))
+                        recs.append(_record(name, strategy, cfg, eng, t, r - a.warmup, threads))
         except Exception as e:  # bench.hpp:182-188: a failed cell becomes a NaN row
             sys.stderr.write(f"{name}: {e}\n")
             recs.append(records.BenchRecord(name, 1, strategy, cfg.num_fish, "gpu", 0, cfg.num_fish,

@@ -93,6 +93,8 @@ SIGNATURES = [
     ("fsb_engine_stream", _int, [_vp, _P(_vp)]),
     ("fsb_engine_time_step_kernels", _int, [_vp, _u64, _u64, _vp]),
     ("fsb_engine_last_launches", _int, [_vp, _P(_u64)]),
+    ("fsb_engine_set_grid", _int, [_vp, _int]),
+    ("fsb_engine_grid", _int, [_vp, _P(_int), _P(_int)]),
     ("fsb_engine_peer_handle", _int, [_vp, _vp, _sz]),
     ("fsb_engine_peer_connect", _int, [_vp, _vp, _sz]),
     ("fsb_selftest_fast_math", _int, [_int, _u64, _u64, _vp]),

@@ -137,6 +137,8 @@ struct fsb_engine {
     double* d_scalar = nullptr;   // [4]
     int* d_mismatch = nullptr;
     int grid = 0;            // grid of the compact-state step kernel in use
+    int grid_auto = 0;       // ... as chosen at creation (SMs x occupancy)
+    int block_cap = 0;       // capacity of block_part (CTA partials)
     int grid_explicit = 0;   // grid of the explicit-cur step kernel
     int grid_coop = 0;       // grid of the cooperative persistent grid kernel
     Partial* d_combined = nullptr;           // [2] grid-kernel step partials
@@ -650,19 +652,17 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     CB(cudaMalloc(&e->s.w, bytes));
     CB(cudaMalloc(&e->s.p, bytes));
     e->s.c = nullptr;
-    {
-        // The bulk ring pays a fill/drain per CTA: use it only when every CTA
-        // streams at least 8 sub-tiles (e.g. not for 1e6-fish L2-resident schools).
-        const int grid_bulk = fsb_dev::step_grid_blocks(e->device, false, true);
-        const uint64_t per_cta = (e->count / 2) / (uint64_t)grid_bulk;
-        e->use_bulk = !(e->flags & FSB_FLAG_NO_BULK) &&
-                      (per_cta >= 8ull * fsb_dev::kBulkTilePairs || (e->flags & FSB_FLAG_FORCE_BULK));
-        e->grid = e->use_bulk ? grid_bulk : fsb_dev::step_grid_blocks(e->device, false, false);
-    }
+    // The LDG step kernel is the default: in in-range mode it measured 2-3%
+    // faster than the cp.async.bulk ring at 1e7 and 1e8 fish and 25% faster at
+    // 1e6 (profiles/r03_ab_bulk_ldg.jsonl); the ring stays available for A/B.
+    e->use_bulk = (e->flags & FSB_FLAG_FORCE_BULK) && !(e->flags & FSB_FLAG_NO_BULK);
+    e->grid = fsb_dev::step_grid_blocks(e->device, false, e->use_bulk);
     e->grid_explicit = fsb_dev::step_grid_blocks(e->device, true, false);
     e->grid_coop = fsb_dev::grid_kernel_blocks(e->device);
+    e->grid_auto = e->grid;
     int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
     if (e->grid_coop > maxgrid) maxgrid = e->grid_coop;
+    e->block_cap = maxgrid;
     CB(cudaMalloc(&e->d_combined, 2 * sizeof(Partial)));
     CB(cudaMalloc(&e->d_gen, sizeof(unsigned long long)));
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
@@ -1008,6 +1008,30 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
         CU(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
         kernel_ms[k] = ms;
     }
+    return FSB_OK;
+}
+
+int fsb_engine_set_grid(fsb_engine* e, int ctas) {
+    TRY(guard(e));
+    if (ctas < 0 || ctas > 65536) return fail(FSB_ERR_INVALID_ARGUMENT, "ctas must be in [0, 65536]");
+    const int g = ctas ? ctas : e->grid_auto;
+    if (g > e->block_cap) {
+        CU(cudaStreamSynchronize(e->stream));
+        Partial* nb = nullptr;
+        CU(cudaMalloc(&nb, g * sizeof(Partial)));
+        cudaFree(e->block_part);
+        e->block_part = nb;
+        e->block_cap = g;
+    }
+    if (g != e->grid) free_graphs(e);  // captured launches carry the old grid
+    e->grid = g;
+    return FSB_OK;
+}
+
+int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta) {
+    if (!e) return fail(FSB_ERR_INVALID_ARGUMENT, "null engine");
+    if (ctas) *ctas = e->grid;
+    if (threads_per_cta) *threads_per_cta = e->use_bulk ? fsb_dev::kBulkThreads : fsb_dev::kThreads;
     return FSB_OK;
 }
 

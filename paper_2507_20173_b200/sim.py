@@ -134,13 +134,13 @@ class Engine:
 
     def __init__(self, cfg: SimConfig, device: int = 0, rank: int = 0, world_size: int = 1,
                  nccl_unique_id: Optional[bytes] = None, strategy: str = "auto",
-                 alternate: bool = True, force_nccl: bool = False, bulk=True, pdl: bool = True,
+                 alternate: bool = True, force_nccl: bool = False, bulk=False, pdl: bool = True,
                  peer: bool = False, checked: bool = False):
         self.cfg = cfg
         L = N.lib()
         self._uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
         flags = ((0 if alternate else N.FLAG_NO_ALTERNATE) | (N.FLAG_FORCE_NCCL if force_nccl else 0)
-                 | (0 if bulk else N.FLAG_NO_BULK) | (N.FLAG_FORCE_BULK if bulk == "force" else 0)
+                 | (N.FLAG_FORCE_BULK if bulk else 0)
                  | (0 if pdl else N.FLAG_NO_PDL) | (N.FLAG_PEER_EXCHANGE if peer else 0)
                  | (N.FLAG_CHECKED if checked else 0))
         opts = N.fsb_engine_options(device, rank, world_size,
@@ -257,6 +257,16 @@ class Engine:
         ms = np.empty(num_steps, dtype=np.float64)
         N.check(N.lib().fsb_engine_time_step_kernels(self._h, first_step, num_steps, _ptr(ms)))
         return ms
+
+    def set_grid(self, ctas: int = 0) -> None:
+        """CTA count of the compact step / eat kernels (0 = automatic)."""
+        N.check(N.lib().fsb_engine_set_grid(self._h, ctas))
+
+    def grid(self):
+        """(CTAs, threads per CTA) of the compact step kernel in use."""
+        c, t = ctypes.c_int(), ctypes.c_int()
+        N.check(N.lib().fsb_engine_grid(self._h, ctypes.byref(c), ctypes.byref(t)))
+        return c.value, t.value
 
     def last_launches(self) -> int:
         v = ctypes.c_uint64()

@@ -311,6 +311,24 @@ def test_config_outside_in_range_bounds(orc, over):
         assert eng.download().tobytes() == want_fish.tobytes()
 
 
+@pytest.mark.parametrize("bulk", [False, "force"])
+def test_grid_override_bit_exact(orc, bulk):
+    """fsb_engine_set_grid (the CTA-count sweep): any grid, including more CTAs
+    than 64-pair blocks, gives the oracle's state and trace."""
+    cfg = fsb.baseline_config(100_003, 6)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "stream", bulk=bulk) as eng:
+        auto = eng.grid()
+        for ctas in (1, 7, 148, 1000, 5000, 0):
+            eng.set_grid(ctas)
+            assert eng.grid()[0] == (ctas or auto[0])
+            trace, _, _ = eng.simulate(barycentre=False)
+            assert trace.tobytes() == want_trace.tobytes(), ctas
+            assert eng.download().tobytes() == want_fish.tobytes(), ctas
+        with pytest.raises(fsb.FsbError):
+            eng.set_grid(-1)
+
+
 def test_long_stream_run_is_chunked(orc):
     """A run longer than one graph (1024 steps) goes through several graphs."""
     cfg = fsb.baseline_config(20_000, 2500)
@@ -491,7 +509,9 @@ def test_cli_simulate_record(tmp_path, capsys):
     assert cli_main(["gpuexp", "--fish", "4096", "--steps", "50", "--reps", "2", "--warmup", "1",
                      "--out", str(out)]) == 0
     recs = records.read_csv(out.read_text())
-    assert len(recs) == 6 and len({r.checksum for r in recs}) == 1 and not any(r.failed() for r in recs)
+    assert len(recs) == 14 and len({r.checksum for r in recs}) == 1 and not any(r.failed() for r in recs)
+    grid = [r for r in recs if r.experiment == "gpu-grid"]
+    assert len({r.threads for r in grid}) == 4  # 1, 2, 4, 8 CTAs per SM
 
 
 def test_gather_matches_download(orc):

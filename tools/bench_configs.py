@@ -35,7 +35,7 @@ def peak():
         return 6650.0
 
 
-def time_cfg(name, n, t, strategy, alternate, reps, bulk=True, pdl=True, checked=False):
+def time_cfg(name, n, t, strategy, alternate, reps, bulk=False, pdl=True, checked=False):
     cfg = fsb.baseline_config(n, t)
     with fsb.Engine(cfg, strategy=strategy, alternate=alternate, bulk=bulk, pdl=pdl, checked=checked) as eng:
         eng.init()
@@ -59,29 +59,29 @@ def main():
     ap.add_argument("--only", default="C0,C1,C2,C3,C4")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--variants", action="store_true", help="also stream/persistent and alternate on/off")
-    ap.add_argument("--bulk-ab", action="store_true", help="also the LDG step kernel (no bulk ring)")
+    ap.add_argument("--bulk-ab", action="store_true", help="also the cp.async.bulk ring step kernel")
     ap.add_argument("--pdl-ab", action="store_true", help="also without programmatic dependent launch")
     ap.add_argument("--grid-ab", action="store_true", help="also the persistent cooperative-grid strategy")
     ap.add_argument("--checked-ab", action="store_true", help="also with the fp64 guards always evaluated")
     a = ap.parse_args()
     for name in a.only.split(","):
         n, t = CONFIGS[name]
-        plans = [("auto", True, True)]
+        plans = [("auto", True, False)]
         if a.bulk_ab and n > 32768:
-            plans += [("stream", True, False)]
+            plans += [("stream", True, True)]
         if a.variants:
-            plans += [("stream", False, True), ("stream", True, False)]
+            plans += [("stream", False, False)]
             if n <= 32768:
-                plans += [("stream", True, True), ("persistent", True, True)]
+                plans += [("stream", True, False), ("persistent", True, False)]
         for strategy, alt, bulk in plans:
             print(json.dumps(time_cfg(name, n, t, strategy, alt, a.reps, bulk)), flush=True)
         if a.pdl_ab and n > 32768:
-            print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, True, pdl=False)), flush=True)
+            print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, False, pdl=False)), flush=True)
         if a.checked_ab and n > 32768:
             for bulk in (True, False):
                 print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, bulk, checked=True)), flush=True)
         if a.grid_ab and n > 16384:
-            print(json.dumps(time_cfg(name, n, t, "grid", True, a.reps, True)), flush=True)
+            print(json.dumps(time_cfg(name, n, t, "grid", True, a.reps, False)), flush=True)
 
 
 if __name__ == "__main__":
