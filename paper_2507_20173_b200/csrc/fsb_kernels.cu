@@ -421,7 +421,27 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
     double2* P2 = reinterpret_cast<double2*>(a.s.p);
     const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
 
+#if FSB_L2_PREFETCH
+    // One thread keeps FSB_L2_PREFETCH sub-tiles ahead in flight to L2 with
+    // bulk prefetches (no registers, no shared memory), so the warps' loads
+    // hit L2 instead of waiting on DRAM.
+    auto l2_prefetch = [&](uint64_t jj) {
+        const uint64_t sb = lo + (rev ? nsub - 1 - jj : jj) * kTilePairs;
+        const unsigned bytes = (unsigned)(((hi - sb < (uint64_t)kTilePairs) ? hi - sb : kTilePairs) * 16);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X2 + sb), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Y2 + sb), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(W2 + sb), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P2 + sb), "r"(bytes) : "memory");
+        if (kExplicitCur)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(C2 + sb), "r"(bytes) : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (uint64_t d = 0; d < (uint64_t)FSB_L2_PREFETCH && d < nsub; ++d) l2_prefetch(d);
+#endif
     for (uint64_t j = 0; j < nsub; ++j) {
+#if FSB_L2_PREFETCH
+        if (threadIdx.x == 0 && j + FSB_L2_PREFETCH < nsub) l2_prefetch(j + FSB_L2_PREFETCH);
+#endif
         const uint64_t sub = rev ? nsub - 1 - j : j;
         const uint64_t base = lo + sub * kTilePairs + threadIdx.x;
         double2 X[kPairsPerThread], Y[kPairsPerThread], W[kPairsPerThread], Q[kPairsPerThread],
@@ -479,6 +499,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                  : "memory");
 }
 
+template <bool kSane>
 __device__ __forceinline__ void step_chunk_prefetch(const StepArgs& a, const StepParams& P, bool eat,
                                                     const SharedDivisor& M, uint64_t step, Partial& acc) {
     constexpr int S = FSB_LDG_PREFETCH;
@@ -526,7 +547,7 @@ __device__ __forceinline__ void step_chunk_prefetch(const StepArgs& a, const Ste
             W[0] = ring[s][2][t];
             Q[0] = ring[s][3][t];
         }
-        fused_pairs<false, 1, false>(X, Y, W, Q, X, valid, src, qs, gi, P, eat, M, step, acc);
+        fused_pairs<false, 1, kSane>(X, Y, W, Q, X, valid, src, qs, gi, P, eat, M, step, acc);
         if (valid[0]) {
             X2[q] = X[0];
             Y2[q] = Y[0];
@@ -558,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
     Partial acc = identity();
 #if FSB_LDG_PREFETCH
-    if (!kExplicitCur) step_chunk_prefetch(a, P, eat, M, step, acc);
+    if (!kExplicitCur) step_chunk_prefetch<kSane>(a, P, eat, M, step, acc);
     else
 #endif
         step_chunk<kExplicitCur, kSane>(a, P, eat, M, step, acc);

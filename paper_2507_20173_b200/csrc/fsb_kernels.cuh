@@ -52,6 +52,9 @@ namespace fsb_dev {
 #ifndef FSB_LDG_PREFETCH
 #define FSB_LDG_PREFETCH 0  // >1: LDG step kernel prefetches through a per-thread cp.async ring
 #endif
+#ifndef FSB_L2_PREFETCH
+#define FSB_L2_PREFETCH 0  // >0: LDG step kernel bulk-prefetches that many sub-tiles ahead into L2
+#endif
 #ifndef FSB_BULK_STORE
 #define FSB_BULK_STORE 1  // 1: results bulk-stored from the stage; 0: STG from registers
 #endif

@@ -33,6 +33,12 @@ VARIANTS = {
     "pf3": ["-DFSB_LDG_PREFETCH=3"],
     "pf4": ["-DFSB_LDG_PREFETCH=4", "-DFSB_MIN_BLOCKS=3"],
     "l2_pf3": ["-DFSB_LDG_PREFETCH=3", "-DFSB_MEM_WINDOW=512"],
+    # LDG kernel with cp.async.bulk.prefetch.L2 of the sub-tile D ahead (one thread per CTA)
+    "l2pf1": ["-DFSB_L2_PREFETCH=1"],
+    "l2pf2": ["-DFSB_L2_PREFETCH=2"],
+    "l2pf4": ["-DFSB_L2_PREFETCH=4"],
+    "l2pf8": ["-DFSB_L2_PREFETCH=8"],
+    "l2pf4_p2b3": ["-DFSB_L2_PREFETCH=4", "-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=3"],
     # bulk ring with direct STG stores (stage released right after the LDS)
     "stg": ["-DFSB_BULK_STORE=0"],
     "stg_b2s3m2": ["-DFSB_BULK_STORE=0", "-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=3", "-DFSB_BULK_MIN_BLOCKS=2"],
