@@ -110,11 +110,31 @@ class FsbError(RuntimeError):
 _lib = None
 
 
+def _pin_nccl() -> None:
+    """Point FSB_NCCL_LIB at the NCCL that torch links (the nvidia-nccl wheel),
+    unless the caller chose one: the engine dlopens NCCL lazily, and a different
+    libnccl.so.2 loaded first would shadow torch's by soname."""
+    if os.environ.get("FSB_NCCL_LIB"):
+        return
+    try:
+        import importlib.util
+
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for d in (spec.submodule_search_locations if spec else None) or []:
+            cand = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(cand):
+                os.environ["FSB_NCCL_LIB"] = cand
+                return
+    except Exception:
+        pass
+
+
 def lib() -> ctypes.CDLL:
     """Load (building first if stale) libfsb_b200.so.  FSB_LIB may name a
     prebuilt variant of the same library (tools/variants.py A/B builds)."""
     global _lib
     if _lib is None:
+        _pin_nccl()
         path = os.environ.get("FSB_LIB") or _build.build()
         L = ctypes.CDLL(path)
         for name, res, args in SIGNATURES:

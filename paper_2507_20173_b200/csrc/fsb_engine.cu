@@ -9,6 +9,7 @@
 // (executor.hpp:63-103, 130-159): no host thread touches fish state.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <cstdlib>
 #include <nccl.h>
 
 #include <cmath>
@@ -73,8 +74,17 @@ int nccl_load() {
     if (g_nccl.handle) return FSB_OK;
     if (g_nccl.tried) return fail(FSB_ERR_NCCL, "libnccl.so.2 could not be loaded");
     g_nccl.tried = true;
-    // An already-loaded NCCL (e.g. torch's) is reused through its soname.
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // FSB_NCCL_LIB names the library explicitly.  The Python layer points it
+    // at the NCCL torch itself links, so whichever of the two loads first,
+    // both resolve libnccl.so.2 to the same file; otherwise an already-loaded
+    // NCCL is reused through its soname, else the system one is loaded.
+    void* h = nullptr;
+    const char* path = std::getenv("FSB_NCCL_LIB");
+    if (path && *path) {
+        h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return fail(FSB_ERR_NCCL, std::string("dlopen FSB_NCCL_LIB failed: ") + dlerror());
+    }
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (!h) return fail(FSB_ERR_NCCL, std::string("dlopen libnccl.so.2 failed: ") + dlerror());
     g_nccl.GetUniqueId = reinterpret_cast<decltype(g_nccl.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));

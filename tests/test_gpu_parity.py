@@ -6,6 +6,7 @@ FMA); barycentre sums within 1e-12 relative of the compensated oracle.
 """
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -397,6 +398,21 @@ def test_force_nccl_world1(orc):
         eng.move(8)
         orc.move(ocfg(cfg), 8, want_fish)
         assert bits(eng.eat().max_diff) == bits(orc.eat(ocfg(cfg), want_fish))
+
+
+def test_nccl_before_torch_import():
+    """An NCCL engine created before torch is imported must not shadow the NCCL
+    torch links (libnccl.so.2 is shared by soname): a fresh process creates a
+    FORCE_NCCL engine, then imports torch and runs a CUDA op."""
+    code = ("import paper_2507_20173_b200 as fsb\n"
+            "cfg = fsb.baseline_config(1000, 2)\n"
+            "e = fsb.Engine(cfg, nccl_unique_id=fsb.nccl_unique_id(), force_nccl=True)\n"
+            "e.simulate()\n"
+            "import torch\n"
+            "assert torch.ones(4, device='cuda').sum().item() == 4.0\n"
+            "e.close()\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
 
 
 @pytest.mark.parametrize("n,t", [(100_001, 9), (4096, 30), (1, 5), (0, 3)])
