@@ -421,27 +421,7 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
     double2* P2 = reinterpret_cast<double2*>(a.s.p);
     const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
 
-#if FSB_L2_PREFETCH
-    // One thread keeps FSB_L2_PREFETCH sub-tiles ahead in flight to L2 with
-    // bulk prefetches (no registers, no shared memory), so the warps' loads
-    // hit L2 instead of waiting on DRAM.
-    auto l2_prefetch = [&](uint64_t jj) {
-        const uint64_t sb = lo + (rev ? nsub - 1 - jj : jj) * kTilePairs;
-        const unsigned bytes = (unsigned)(((hi - sb < (uint64_t)kTilePairs) ? hi - sb : kTilePairs) * 16);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X2 + sb), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Y2 + sb), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(W2 + sb), "r"(bytes) : "memory");
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P2 + sb), "r"(bytes) : "memory");
-        if (kExplicitCur)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(C2 + sb), "r"(bytes) : "memory");
-    };
-    if (threadIdx.x == 0)
-        for (uint64_t d = 0; d < (uint64_t)FSB_L2_PREFETCH && d < nsub; ++d) l2_prefetch(d);
-#endif
     for (uint64_t j = 0; j < nsub; ++j) {
-#if FSB_L2_PREFETCH
-        if (threadIdx.x == 0 && j + FSB_L2_PREFETCH < nsub) l2_prefetch(j + FSB_L2_PREFETCH);
-#endif
         const uint64_t sub = rev ? nsub - 1 - j : j;
         const uint64_t base = lo + sub * kTilePairs + threadIdx.x;
         double2 X[kPairsPerThread], Y[kPairsPerThread], W[kPairsPerThread], Q[kPairsPerThread],
@@ -488,85 +468,6 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
     }
 }
 
-#if FSB_LDG_PREFETCH
-// step_chunk with a per-thread cp.async (LDGSTS) prefetch ring: every thread
-// copies ITS OWN pair of the next FSB_LDG_PREFETCH-1 sub-tiles into shared
-// memory while it computes the current one, so the loads in flight cost no
-// registers and need no CTA-wide synchronisation (compact state, 1 pair/thread).
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
-                 "l"(gmem)
-                 : "memory");
-}
-
-template <bool kSane>
-__device__ __forceinline__ void step_chunk_prefetch(const StepArgs& a, const StepParams& P, bool eat,
-                                                    const SharedDivisor& M, uint64_t step, Partial& acc) {
-    constexpr int S = FSB_LDG_PREFETCH;
-    extern __shared__ __align__(16) unsigned char ldg_ring_raw[];  // S x 4 x kThreads double2
-    auto ring = reinterpret_cast<double2(*)[4][kThreads]>(ldg_ring_raw);
-    const uint64_t n = a.n;
-    const uint64_t npairs = n >> 1;
-    const bool rev = a.alternate && (step & 1ull);
-    constexpr uint64_t kAlign = 64;
-    const uint64_t nblk = (npairs + kAlign - 1) / kAlign;
-    const uint64_t lo = (nblk * blockIdx.x / gridDim.x) * kAlign;
-    uint64_t hi = (nblk * (blockIdx.x + 1) / gridDim.x) * kAlign;
-    if (hi > npairs) hi = npairs;
-    const uint64_t nsub = hi > lo ? (hi - lo + kThreads - 1) / kThreads : 0;
-    double2* X2 = reinterpret_cast<double2*>(a.s.x);
-    double2* Y2 = reinterpret_cast<double2*>(a.s.y);
-    double2* W2 = reinterpret_cast<double2*>(a.s.w);
-    double2* P2 = reinterpret_cast<double2*>(a.s.p);
-    const unsigned t = threadIdx.x;
-    auto pair_of = [&](uint64_t j) { return lo + (rev ? nsub - 1 - j : j) * kThreads + t; };
-    auto issue = [&](uint64_t j) {
-        const uint64_t q = pair_of(j);
-        if (q < hi) {
-            const int s = (int)(j % S);
-            cp_async16(&ring[s][0][t], X2 + q);
-            cp_async16(&ring[s][1][t], Y2 + q);
-            cp_async16(&ring[s][2][t], W2 + q);
-            cp_async16(&ring[s][3][t], P2 + q);
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count aligned)
-    };
-    for (int j = 0; j < S - 1; ++j) issue(j);
-    const SoA2 src{X2, Y2, W2, P2, nullptr};
-    for (uint64_t j = 0; j < nsub; ++j) {
-        issue(j + S - 1);
-        asm volatile("cp.async.wait_group %0;" ::"n"(S - 1) : "memory");  // sub-tile j has landed
-        const uint64_t q = pair_of(j);
-        const int s = (int)(j % S);
-        double2 X[1], Y[1], W[1], Q[1];
-        const bool valid[1] = {q < hi};
-        const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
-        if (valid[0]) {
-            X[0] = ring[s][0][t];
-            Y[0] = ring[s][1][t];
-            W[0] = ring[s][2][t];
-            Q[0] = ring[s][3][t];
-        }
-        fused_pairs<false, 1, kSane>(X, Y, W, Q, X, valid, src, qs, gi, P, eat, M, step, acc);
-        if (valid[0]) {
-            X2[q] = X[0];
-            Y2[q] = Y[0];
-            W2[q] = W[0];
-            P2[q] = Q[0];
-        }
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if ((n & 1ull) && blockIdx.x == 0 && t == 0) {  // odd tail fish
-        const uint64_t i = n - 1;
-        double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];
-        fused_fish(x, y, w, p, objective(x, y, P.half_pond), eat, M, a.gfirst + i, step, P, acc);
-        a.s.x[i] = x;
-        a.s.y[i] = y;
-        a.s.w[i] = w;
-        a.s.p[i] = p;
-    }
-}
-#endif
 
 template <bool kExplicitCur, bool kSane>
 __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
@@ -578,11 +479,7 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
     Partial acc = identity();
-#if FSB_LDG_PREFETCH
-    if (!kExplicitCur) step_chunk_prefetch<kSane>(a, P, eat, M, step, acc);
-    else
-#endif
-        step_chunk<kExplicitCur, kSane>(a, P, eat, M, step, acc);
+    step_chunk<kExplicitCur, kSane>(a, P, eat, M, step, acc);
     grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 
@@ -789,7 +686,6 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
             for (uint64_t j = 0; j < nsub; ++j) {
                 const int s = (int)(j % kBulkStages);
                 mbar_wait(&empty[s], (unsigned)((j / kBulkStages) & 1));
-#if FSB_BULK_STORE
                 const uint64_t base = sub_base(j);
                 const uint64_t cnt = (hi - base < (uint64_t)kBulkTilePairs) ? hi - base : (uint64_t)kBulkTilePairs;
                 const unsigned bytes = (unsigned)(cnt * sizeof(double2));
@@ -802,9 +698,6 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     load(j + kBulkStages);
                 }
-#else
-                if (j + kBulkStages < nsub) load(j + kBulkStages);
-#endif
             }
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete before exit
         }
@@ -813,14 +706,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
             const int s = (int)(j % kBulkStages);
             const uint64_t base = sub_base(j);
             mbar_wait(&full[s], (unsigned)((j / kBulkStages) & 1));
-#if FSB_BULK_STORE
             const SoA2 src{stage[s].x, stage[s].y, stage[s].w, stage[s].p, nullptr};
-#else
-            // the stage is released as soon as it is in registers; a guard
-            // fallback re-reads the (not yet overwritten) state from HBM
-            const uint64_t mb = mem_of(base);
-            const SoA2 src{X2 + mb, Y2 + mb, W2 + mb, P2 + mb, nullptr};
-#endif
             double2 X[kBulkPairsPerThread], Y[kBulkPairsPerThread], W[kBulkPairsPerThread], Q[kBulkPairsPerThread];
             bool valid[kBulkPairsPerThread];
             uint64_t ks[kBulkPairsPerThread], gi[kBulkPairsPerThread];
@@ -837,37 +723,22 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
                     Q[u] = stage[s].p[k];
                 }
             }
-#if !FSB_BULK_STORE
-            __syncwarp();
-            if ((t & 31) == 0) mbar_arrive(&empty[s]);
-#endif
             fused_pairs<false, kBulkPairsPerThread, kSane>(X, Y, W, Q, X, valid, src, ks, gi, P, eat, M, step, acc);
 #pragma unroll
             for (int u = 0; u < kBulkPairsPerThread; ++u) {
                 const unsigned k = (unsigned)ks[u];
                 if (valid[u]) {
-#if FSB_BULK_STORE
                     // new state back into the stage, bulk-stored by the producer
                     stage[s].x[k] = X[u];
                     stage[s].y[k] = Y[u];
                     stage[s].w[k] = W[u];
                     stage[s].p[k] = Q[u];
-#else
-                    // new state straight to HBM
-                    const uint64_t q = mem_of(base + k);
-                    X2[q] = X[u];
-                    Y2[q] = Y[u];
-                    W2[q] = W[u];
-                    P2[q] = Q[u];
-#endif
                 }
             }
-#if FSB_BULK_STORE
             // make the generic-proxy smem writes visible to the bulk-store (async) proxy
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if ((t & 31) == 0) mbar_arrive(&empty[s]);
-#endif
         }
         if ((n & 1ull) && blockIdx.x == 0 && t == 0) {  // odd tail fish
             const uint64_t i = n - 1;
@@ -882,61 +753,6 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
     grid_finish(acc, a.ws, a.part_out, a.px, a.world);
 }
 
-#if FSB_SINGLE
-// Experiment (tools/variants.py "single*"): one fish per thread, scalar
-// loads -- maximum thread-level parallelism, minimum registers per thread.
-__global__ void __launch_bounds__(kThreads, FSB_SINGLE_MIN_BLOCKS) step_kernel_single(const StepArgs a) {
-    const StepParams P = params_of(a.k);
-    pdl_wait_and_release();
-    const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out);
-    const bool eat = prev.best > 0.0;
-    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
-    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
-    const uint64_t n = a.n;
-    const bool rev = a.alternate && (step & 1ull);
-    constexpr uint64_t kAlign = 128;
-    const uint64_t nblk = (n + kAlign - 1) / kAlign;
-    const uint64_t lo = (nblk * blockIdx.x / gridDim.x) * kAlign;
-    uint64_t hi = (nblk * (blockIdx.x + 1) / gridDim.x) * kAlign;
-    if (hi > n) hi = n;
-    const uint64_t nsub = hi > lo ? (hi - lo + kThreads - 1) / kThreads : 0;
-    Partial acc = identity();
-    for (uint64_t j = 0; j < nsub; ++j) {
-        const uint64_t i = lo + (rev ? nsub - 1 - j : j) * kThreads + threadIdx.x;
-        bool ok = true;
-        double x = 0, y = 0, w = 0, p = 0, cn = 0;
-        if (i < hi) {
-            x = a.s.x[i];
-            y = a.s.y[i];
-            w = a.s.w[i];
-            p = a.s.p[i];
-            const double c = objective_guarded(x, y, P.half_pond, ok);
-            cn = fused_fish_guarded<false>(x, y, w, p, c, eat, M, a.gfirst + i, step, P, ok);
-        }
-        if (__any_sync(0xffffffffu, !ok)) {
-            if (!ok) {
-                const double x0 = a.s.x[i], y0 = a.s.y[i];
-                const FishOut f = fused_fish_exact(x0, y0, a.s.w[i], a.s.p[i], objective(x0, y0, P.half_pond),
-                                                   eat, M.b, a.gfirst + i, step, P);
-                x = f.x;
-                y = f.y;
-                w = f.w;
-                p = f.p;
-                cn = f.cn;
-            }
-        }
-        if (i < hi) {
-            accumulate(acc, x, y, p, cn);
-            a.s.x[i] = x;
-            a.s.y[i] = y;
-            a.s.w[i] = w;
-            a.s.p[i] = p;
-        }
-    }
-    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
-}
-#endif
 
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
@@ -1236,17 +1052,8 @@ int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
                                                           kBulkSmemBytes);
     } else {
         e = explicit_cur
-            ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true, false>, kThreads, 0)
-#if FSB_SINGLE
-            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_single, kThreads, 0);
-#else
-            : (cudaFuncSetAttribute(step_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kLdgRingBytes),
-               cudaFuncSetAttribute(step_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    kLdgRingBytes),
-               cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false, false>, kThreads,
-                                                             kLdgRingBytes));
-#endif
+                ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true, false>, kThreads, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false, false>, kThreads, 0);
     }
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     return num_sms(device) * per_sm;
@@ -1289,12 +1096,8 @@ cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
     if (a.bulk)
         return launch_maybe_pdl(sane ? step_kernel_bulk<true> : step_kernel_bulk<false>, grid, kBulkThreads,
                                 kBulkSmemBytes, st, a, pdl);
-#if FSB_SINGLE
-    return launch_maybe_pdl(step_kernel_single, grid, kThreads, 0, st, a, pdl);
-#else
-    return launch_maybe_pdl(sane ? step_kernel<false, true> : step_kernel<false, false>, grid, kThreads,
-                            kLdgRingBytes, st, a, pdl);
-#endif
+    return launch_maybe_pdl(sane ? step_kernel<false, true> : step_kernel<false, false>, grid, kThreads, 0, st, a,
+                            pdl);
 }
 
 cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st) {

@@ -32,12 +32,6 @@ namespace fsb_dev {
 #define FSB_MEM_WINDOW 0
 #endif
 
-#ifndef FSB_SINGLE
-#define FSB_SINGLE 0  // experiment: one fish per thread in the LDG step kernel
-#endif
-#ifndef FSB_SINGLE_MIN_BLOCKS
-#define FSB_SINGLE_MIN_BLOCKS 6
-#endif
 
 #ifndef FSB_CLUSTER_MIN_FISH
 #define FSB_CLUSTER_MIN_FISH 256  // persistent kernel: fish per CTA before adding CTAs
@@ -49,15 +43,6 @@ namespace fsb_dev {
 #ifndef FSB_BULK_MIN_BLOCKS
 #define FSB_BULK_MIN_BLOCKS 3
 #endif
-#ifndef FSB_LDG_PREFETCH
-#define FSB_LDG_PREFETCH 0  // >1: LDG step kernel prefetches through a per-thread cp.async ring
-#endif
-#ifndef FSB_L2_PREFETCH
-#define FSB_L2_PREFETCH 0  // >0: LDG step kernel bulk-prefetches that many sub-tiles ahead into L2
-#endif
-#ifndef FSB_BULK_STORE
-#define FSB_BULK_STORE 1  // 1: results bulk-stored from the stage; 0: STG from registers
-#endif
 #ifndef FSB_BULK_PAIRS
 #define FSB_BULK_PAIRS 1
 #endif
@@ -66,7 +51,6 @@ constexpr int kThreads = 256;     // threads per CTA of the streaming kernels
 constexpr int kPairsPerThread = FSB_PAIRS;  // double2 loads per array per thread per tile
 constexpr int kTilePairs = kThreads * kPairsPerThread;
 constexpr int kTileFish = 2 * kTilePairs;
-constexpr int kLdgRingBytes = FSB_LDG_PREFETCH * 4 * kThreads * 16;  // dynamic smem of step_kernel<false>
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,
 // plus one producer warp; a kBulkStages-deep ring of sub-tiles in smem.

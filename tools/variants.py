@@ -5,6 +5,9 @@
     python tools/variants.py run [--only C1]  # on the GPU box: bench_configs per variant
 
 Variants live in build/variants/ (git-ignored, travels to the GPU box).
+Experiments that lost and were removed from the sources after measurement
+(per-thread cp.async prefetch ring, L2 bulk prefetch, bulk ring with STG
+stores, IMAD.HI shifts, one fish per thread) are in profiles/r0*_variants.jsonl.
 """
 from __future__ import annotations
 
@@ -28,29 +31,7 @@ VARIANTS = {
     "b1s4m3": ["-DFSB_BULK_PAIRS=1", "-DFSB_BULK_STAGES=4", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b4s2m1": ["-DFSB_BULK_PAIRS=4", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=1"],
-    # LDG kernel with a per-thread cp.async prefetch ring of S sub-tiles
-    "pf2": ["-DFSB_LDG_PREFETCH=2"],
-    "pf3": ["-DFSB_LDG_PREFETCH=3"],
-    "pf4": ["-DFSB_LDG_PREFETCH=4", "-DFSB_MIN_BLOCKS=3"],
-    "l2_pf3": ["-DFSB_LDG_PREFETCH=3", "-DFSB_MEM_WINDOW=512"],
-    # LDG kernel with cp.async.bulk.prefetch.L2 of the sub-tile D ahead (one thread per CTA)
-    "l2pf1": ["-DFSB_L2_PREFETCH=1"],
-    "l2pf2": ["-DFSB_L2_PREFETCH=2"],
-    "l2pf4": ["-DFSB_L2_PREFETCH=4"],
-    "l2pf8": ["-DFSB_L2_PREFETCH=8"],
-    "l2pf4_p2b3": ["-DFSB_L2_PREFETCH=4", "-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=3"],
-    # bulk ring with direct STG stores (stage released right after the LDS)
-    "stg": ["-DFSB_BULK_STORE=0"],
-    "stg_b2s3m2": ["-DFSB_BULK_STORE=0", "-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=3", "-DFSB_BULK_MIN_BLOCKS=2"],
-    "l2_stg": ["-DFSB_BULK_STORE=0", "-DFSB_MEM_WINDOW=512"],
     "l2_bulk": ["-DFSB_MEM_WINDOW=512"],
-    # RNG high-word shifts on the fma pipe (IMAD.HI) instead of the alu pipe
-    "imadsh": ["-DFSB_IMAD_SHIFTS=1"],
-    "imadsh_p2b3": ["-DFSB_IMAD_SHIFTS=1", "-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=3"],
-    # LDG kernel, one fish per thread
-    "single4": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=4"],
-    "single6": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=6"],
-    "single8": ["-DFSB_SINGLE=1", "-DFSB_SINGLE_MIN_BLOCKS=8"],
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
