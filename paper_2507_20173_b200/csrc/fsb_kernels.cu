@@ -6,6 +6,10 @@
 //                   objective (sim.hpp:90-98), and this step's partial
 //                   max(prev-cur) (sim.hpp:112-114) plus the f-weighted
 //                   barycentre sums, reduced warp -> CTA -> grid (last CTA).
+//                   double2 loads/stores, two fish per thread (the default).
+//   step_kernel_bulk  the same pass streamed through a shared-memory ring by
+//                   cp.async.bulk + mbarriers (FSB_FLAG_FORCE_BULK, A/B).
+//   grid_kernel     all T steps in one cooperative launch (FSB_STRATEGY_GRID).
 //   eat_kernel      the trailing / standalone weight update (sim.hpp:115-121).
 //   reduce_kernel   max + sums of the current state without moving it (eat()
 //                   after an upload).
