@@ -1041,7 +1041,7 @@ int fsb_engine_set_grid(fsb_engine* e, int ctas) {
 int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta) {
     if (!e) return fail(FSB_ERR_INVALID_ARGUMENT, "null engine");
     if (ctas) *ctas = e->grid;
-    if (threads_per_cta) *threads_per_cta = e->use_bulk ? fsb_dev::kBulkThreads : fsb_dev::kThreads;
+    if (threads_per_cta) *threads_per_cta = e->use_bulk ? fsb_dev::kBulkThreads : fsb_dev::kStepThreads;
     return FSB_OK;
 }
 

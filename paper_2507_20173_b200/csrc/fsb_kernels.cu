@@ -434,7 +434,7 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
         uint64_t qs[kPairsPerThread], gi[kPairsPerThread];
 #pragma unroll
         for (int u = 0; u < kPairsPerThread; ++u) {
-            const uint64_t qq = base + (uint64_t)u * kThreads;
+            const uint64_t qq = base + (uint64_t)u * kStepThreads;
             const uint64_t q = FSB_MEM_WINDOW ? lo + ((qq - lo) % FSB_MEM_WINDOW) : qq;
             qs[u] = q;
             gi[u] = a.gfirst + 2 * qq;
@@ -474,7 +474,7 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
 
 
 template <bool kExplicitCur, bool kSane>
-__global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
     const StepParams P = params_of(a.k);
     pdl_wait_and_release();
     const Partial prev = combine_prev(a.part_in, a.world, a.px);
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) step_kernel(const St
 // others sleep on the generation word.  Co-residency of all CTAs is
 // guaranteed by the cooperative launch.
 template <bool kSane>
-__global__ void __launch_bounds__(kThreads, FSB_MIN_BLOCKS) grid_kernel(const GridArgs g) {
+__global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(const GridArgs g) {
     const StepArgs& a = g.base;
     const StepParams P = params_of(a.k);
     __shared__ Partial scratch[32];
@@ -1056,8 +1056,8 @@ int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
                                                           kBulkSmemBytes);
     } else {
         e = explicit_cur
-                ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true, false>, kThreads, 0)
-                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false, false>, kThreads, 0);
+                ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<true, false>, kStepThreads, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel<false, false>, kStepThreads, 0);
     }
     if (e != cudaSuccess || per_sm < 1) per_sm = 1;
     return num_sms(device) * per_sm;
@@ -1095,12 +1095,12 @@ cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
     const bool pdl = a.pdl != 0;
     const bool sane = a.sane != 0;
     if (a.s.c)
-        return launch_maybe_pdl(sane ? step_kernel<true, true> : step_kernel<true, false>, grid, kThreads, 0, st,
+        return launch_maybe_pdl(sane ? step_kernel<true, true> : step_kernel<true, false>, grid, kStepThreads, 0, st,
                                 a, pdl);
     if (a.bulk)
         return launch_maybe_pdl(sane ? step_kernel_bulk<true> : step_kernel_bulk<false>, grid, kBulkThreads,
                                 kBulkSmemBytes, st, a, pdl);
-    return launch_maybe_pdl(sane ? step_kernel<false, true> : step_kernel<false, false>, grid, kThreads, 0, st, a,
+    return launch_maybe_pdl(sane ? step_kernel<false, true> : step_kernel<false, false>, grid, kStepThreads, 0, st, a,
                             pdl);
 }
 
@@ -1113,8 +1113,8 @@ cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st) {
 int grid_kernel_blocks(int device) {
     // co-residency of every CTA: the smaller occupancy of the two instantiations
     int per_sm = 0, per_sm_sane = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_kernel<false>, kThreads, 0) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sane, grid_kernel<true>, kThreads, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_kernel<false>, kStepThreads, 0) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_sane, grid_kernel<true>, kStepThreads, 0) !=
             cudaSuccess) {
         cudaGetLastError();
         per_sm = per_sm_sane = 1;
@@ -1127,7 +1127,7 @@ cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st) {
     void* args[] = {const_cast<GridArgs*>(&g)};
     const void* kern = g.base.sane ? reinterpret_cast<const void*>(grid_kernel<true>)
                                    : reinterpret_cast<const void*>(grid_kernel<false>);
-    return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kThreads), args,
+    return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kStepThreads), args,
                                        0, st);
 }
 

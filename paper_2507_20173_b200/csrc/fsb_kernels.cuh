@@ -47,9 +47,14 @@ namespace fsb_dev {
 #define FSB_BULK_PAIRS 1
 #endif
 
+#ifndef FSB_STEP_THREADS
+#define FSB_STEP_THREADS 256
+#endif
+
 constexpr int kThreads = 256;     // threads per CTA of the streaming kernels
+constexpr int kStepThreads = FSB_STEP_THREADS;  // ... of the LDG step kernel and the grid kernel
 constexpr int kPairsPerThread = FSB_PAIRS;  // double2 loads per array per thread per tile
-constexpr int kTilePairs = kThreads * kPairsPerThread;
+constexpr int kTilePairs = kStepThreads * kPairsPerThread;
 constexpr int kTileFish = 2 * kTilePairs;
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,
