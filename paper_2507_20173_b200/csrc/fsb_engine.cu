@@ -151,8 +151,7 @@ struct fsb_engine {
     int block_cap = 0;       // capacity of block_part (CTA partials)
     int grid_explicit = 0;   // grid of the explicit-cur step kernel
     int grid_coop = 0;       // grid of the cooperative persistent grid kernel
-    Partial* d_combined = nullptr;           // [2] grid-kernel step partials
-    unsigned long long* d_gen = nullptr;     // grid-kernel generation word
+    unsigned long long* d_gen = nullptr;     // grid-kernel arrival counter
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
 
     void* staging = nullptr;  // device AoS staging
@@ -398,7 +397,6 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
     g.num_steps = T;
     g.trace = e->d_cl_trace;
     g.bary = bary ? e->d_cl_bary : nullptr;
-    g.combined = e->d_combined;
     g.gen = e->d_gen;
     CU(cudaMemsetAsync(e->d_gen, 0, sizeof(unsigned long long), e->stream));
     CU(cudaEventRecord(e->ev0, e->stream));
@@ -587,8 +585,7 @@ int fsb_engine_destroy(fsb_engine* e) {
     for (void* p : e->opened) cudaIpcCloseMemHandle(p);
     if (e->window) cudaFree(e->window);
     if (e->d_peers) cudaFree(e->d_peers);
-    for (void* p : {(void*)e->d_combined, (void*)e->d_gen})
-        if (p) cudaFree(p);
+    if (e->d_gen) cudaFree(e->d_gen);
     for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
                     (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
                     (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
@@ -672,8 +669,8 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     e->grid_auto = e->grid;
     int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
     if (e->grid_coop > maxgrid) maxgrid = e->grid_coop;
+    if (2 * e->grid_coop > maxgrid) maxgrid = 2 * e->grid_coop;  // grid kernel: two slot sets
     e->block_cap = maxgrid;
-    CB(cudaMalloc(&e->d_combined, 2 * sizeof(Partial)));
     CB(cudaMalloc(&e->d_gen, sizeof(unsigned long long)));
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));

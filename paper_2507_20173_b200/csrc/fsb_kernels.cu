@@ -500,7 +500,6 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
     const StepArgs& a = g.base;
     const StepParams P = params_of(a.k);
     __shared__ Partial scratch[32];
-    __shared__ bool am_last;
     __shared__ Partial shared_prev;
     Partial prev = identity();  // no pending eat at the start of a run
     for (uint64_t k = 0; k < g.num_steps; ++k) {
@@ -510,34 +509,34 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
         Partial acc = identity();
         step_chunk<false, kSane>(a, P, eat, M, step, acc);
         const Partial blk = block_reduce(acc, scratch);
+        // Grid exchange: publish the CTA partial into slot [k&1][b], arrive on
+        // the monotonic counter, wait for all G arrivals of this step, then
+        // EVERY CTA folds the G partials itself in index order (the same tree
+        // as grid_finish, so every CTA -- and the stream path -- gets the same
+        // bits).  Two slot sets suffice: a CTA rewrites set k&1 at step k+2
+        // only after every CTA has arrived at step k+1, i.e. finished reading.
+        Partial* slots = a.ws.block_part + (k & 1) * gridDim.x;
         if (threadIdx.x == 0) {
-            store_partial(&a.ws.block_part[blockIdx.x], blk);
+            store_partial(&slots[blockIdx.x], blk);
             __threadfence();
-            am_last = atomicAdd(a.ws.counter, 1u) == gridDim.x - 1;
+            atomicAdd(g.gen, 1ull);
+            const unsigned long long target = (k + 1) * (unsigned long long)gridDim.x;
+            while (ld_acquire_gpu(g.gen) < target) __nanosleep(20);
         }
         __syncthreads();
-        if (am_last) {
-            __threadfence();
-            Partial t = identity();
-            for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) fold(t, load_cg(&a.ws.block_part[i]));
-            __syncthreads();
-            const Partial tot = block_reduce(t, scratch);
-            if (threadIdx.x == 0) {
-                shared_prev = tot;
+        Partial t = identity();
+        for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) fold(t, load_cg(&slots[i]));
+        const Partial tot = block_reduce(t, scratch);
+        if (threadIdx.x == 0) {
+            shared_prev = tot;
+            if (blockIdx.x == 0) {
                 g.trace[k] = tot.best;
                 if (g.bary) {
                     g.bary[3 * k + 0] = tot.sx;
                     g.bary[3 * k + 1] = tot.sy;
                     g.bary[3 * k + 2] = tot.sf;
                 }
-                store_partial(&g.combined[k & 1], tot);
-                *a.ws.counter = 0u;
-                __threadfence();
-                st_release_gpu(g.gen, k + 1);  // open generation k+1
             }
-        } else if (threadIdx.x == 0) {
-            while (ld_acquire_gpu(g.gen) != k + 1) __nanosleep(32);
-            shared_prev = load_cg(&g.combined[k & 1]);
         }
         __syncthreads();
         prev = shared_prev;

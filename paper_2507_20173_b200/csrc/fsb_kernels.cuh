@@ -149,8 +149,7 @@ struct GridArgs {
     uint64_t num_steps;
     double* trace;              // [num_steps]
     double* bary;               // [3*num_steps] or nullptr
-    Partial* combined;          // [2] step partial by parity
-    unsigned long long* gen;    // generation word, zero at launch
+    unsigned long long* gen;    // arrival counter, zero at launch; base.ws.block_part holds 2 x grid slots
 };
 
 struct EatArgs {
