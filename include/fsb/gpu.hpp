@@ -203,6 +203,13 @@ class Engine {
     void peer_connect(const std::vector<unsigned char>& all_handles) {
         check(fsb_engine_peer_connect(e_.get(), all_handles.data(), all_handles.size()));
     }
+    // CTA count of the step kernel for configuration sweeps (0 = automatic).
+    void set_grid(int ctas) { check(fsb_engine_set_grid(e_.get(), ctas)); }
+    int grid() const {
+        int ctas = 0;
+        check(fsb_engine_grid(e_.get(), &ctas, nullptr));
+        return ctas;
+    }
 
   private:
     struct Del {
