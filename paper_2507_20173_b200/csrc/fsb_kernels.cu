@@ -509,6 +509,10 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
         Partial acc = identity();
         step_chunk<false, kSane>(a, P, eat, M, step, acc);
         const Partial blk = block_reduce(acc, scratch);
+#if FSB_GRID_TIMING
+        unsigned long long ts0 = 0, ts1 = 0;
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
+#endif
         // Grid exchange: publish the CTA partial into slot [k&1][b], arrive on
         // the monotonic counter, wait for all G arrivals of this step, then
         // EVERY CTA folds the G partials itself in index order (the same tree
@@ -522,6 +526,9 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
             atomicAdd(g.gen, 1ull);
             const unsigned long long target = (k + 1) * (unsigned long long)gridDim.x;
             while (ld_acquire_gpu(g.gen) < target) __nanosleep(20);
+#if FSB_GRID_TIMING
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts1));
+#endif
         }
         __syncthreads();
         Partial t = identity();
@@ -531,11 +538,23 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
             shared_prev = tot;
             if (blockIdx.x == 0) {
                 g.trace[k] = tot.best;
+#if FSB_GRID_TIMING
+                // experiment: CTA 0's globaltimer after its chunk, after the
+                // barrier and after the fold, in place of the barycentre sums
+                unsigned long long ts2;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2));
+                if (g.bary) {
+                    g.bary[3 * k + 0] = __longlong_as_double((long long)ts0);
+                    g.bary[3 * k + 1] = __longlong_as_double((long long)ts1);
+                    g.bary[3 * k + 2] = __longlong_as_double((long long)ts2);
+                }
+#else
                 if (g.bary) {
                     g.bary[3 * k + 0] = tot.sx;
                     g.bary[3 * k + 1] = tot.sy;
                     g.bary[3 * k + 2] = tot.sf;
                 }
+#endif
             }
         }
         __syncthreads();

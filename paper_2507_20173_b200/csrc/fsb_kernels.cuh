@@ -37,6 +37,9 @@ namespace fsb_dev {
 #define FSB_CLUSTER_MIN_FISH 256  // persistent kernel: fish per CTA before adding CTAs
 #endif
 
+#ifndef FSB_GRID_TIMING
+#define FSB_GRID_TIMING 0  // experiment: grid kernel records CTA 0's phase timestamps in place of bary
+#endif
 #ifndef FSB_BULK_STAGES
 #define FSB_BULK_STAGES 4
 #endif
