@@ -84,6 +84,9 @@ enum fsb_strategy {
 #define FSB_FLAG_NO_PDL 0x10u      /* no Programmatic Dependent Launch between graph step kernels */
 #define FSB_FLAG_PEER_EXCHANGE 0x20u /* per-step exchange by NVLink peer stores from the step kernel
                                         itself (CUDA IPC windows) instead of an NCCL allgather */
+#define FSB_FLAG_STATIC_TILES 0x80u  /* LDG step kernel: one static chunk per 256-thread CTA, 4 CTAs per SM */
+#define FSB_FLAG_DYNAMIC_TILES 0x100u /* LDG step kernel: one 1024-thread CTA per SM whose warps claim tiles
+                                        (default: dynamic from 2e7 fish per shard) */
 #define FSB_FLAG_CHECKED 0x40u     /* always evaluate the fp64 fast-path operand guards (default: elided
                                       while config and state are provably in range; results identical) */
 

@@ -31,6 +31,8 @@ FLAG_FORCE_BULK = 0x8
 FLAG_NO_PDL = 0x10
 FLAG_PEER_EXCHANGE = 0x20
 FLAG_CHECKED = 0x40
+FLAG_STATIC_TILES = 0x80
+FLAG_DYNAMIC_TILES = 0x100
 
 
 class fsb_sim_config(ctypes.Structure):

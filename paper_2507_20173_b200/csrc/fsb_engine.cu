@@ -106,6 +106,9 @@ int nccl_fail(ncclResult_t r, const char* what) {
 }
 
 constexpr uint64_t kStagingFish = 1ull << 22;  // 160 MB AoS staging per chunk
+// Shards from this size take step_kernel_dyn (3-5% faster from 5e7 fish, even
+// at 1e7-2e7, slower on L2-resident schools: profiles/r03_ab_kernels.jsonl).
+constexpr uint64_t kDynamicMinFish = 20000000;
 
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
@@ -150,6 +153,8 @@ struct fsb_engine {
     int grid_auto = 0;       // ... as chosen at creation (SMs x occupancy)
     int block_cap = 0;       // capacity of block_part (CTA partials)
     int grid_explicit = 0;   // grid of the explicit-cur step kernel
+    int grid_aux = 0;        // grid of the eat / reduce kernels (SMs x occupancy, 256 threads)
+    bool use_dyn = false;    // compact LDG step: step_kernel_dyn (one CTA per SM, claimed tiles)
     int grid_coop = 0;       // grid of the cooperative persistent grid kernel
     unsigned long long* d_gen = nullptr;     // grid-kernel arrival counter
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
@@ -279,6 +284,7 @@ fsb_dev::StepArgs step_args(fsb_engine* e, const fsb_dev::SoA& s) {
     a.ws.counter = e->counter;
     a.alternate = (e->flags & FSB_FLAG_NO_ALTERNATE) ? 0 : 1;
     a.bulk = e->use_bulk ? 1 : 0;
+    a.dyn = e->use_dyn ? 1 : 0;
     a.sane = in_range(e) ? 1 : 0;
     return a;
 }
@@ -329,7 +335,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         ea.bary_out = g.d_bary + 3 * (T - 1);
         ea.px = px_of(e, e->d_step0 + 1, T, 0);
         ea.pdl = use_pdl(e) ? 1 : 0;
-        ce = fsb_dev::launch_eat(ea, e->grid, e->stream);
+        ce = fsb_dev::launch_eat(ea, e->grid_aux, e->stream);
         ++launches;
     }
     cudaGraph_t graph = nullptr;
@@ -463,7 +469,7 @@ int reduce_current(fsb_engine* e) {
     a.px = px_of(e, nullptr, 0, e->xseq + 1);
     // launched even for an empty shard: it publishes the identity partial (and,
     // with a peer exchange, pushes it so the other ranks are not kept waiting)
-    CU(fsb_dev::launch_reduce(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
+    CU(fsb_dev::launch_reduce(a, e->grid_aux, e->stream));
     TRY(exchange(e, 0));
     e->cur_buf = 0;
     e->max_valid = e->sums_valid = true;
@@ -663,11 +669,18 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     // faster than the cp.async.bulk ring at 1e7 and 1e8 fish and 25% faster at
     // 1e6 (profiles/r03_ab_bulk_ldg.jsonl); the ring stays available for A/B.
     e->use_bulk = (e->flags & FSB_FLAG_FORCE_BULK) && !(e->flags & FSB_FLAG_NO_BULK);
-    e->grid = fsb_dev::step_grid_blocks(e->device, false, e->use_bulk);
-    e->grid_explicit = fsb_dev::step_grid_blocks(e->device, true, false);
+    // claimed tiles only where they measured faster (large shards); the
+    // static chunks win on L2-resident schools (profiles/r03_ab_kernels.jsonl)
+    e->use_dyn = !e->use_bulk && !(e->flags & FSB_FLAG_STATIC_TILES) &&
+                 ((e->flags & FSB_FLAG_DYNAMIC_TILES) || e->count >= kDynamicMinFish);
+    e->grid_aux = fsb_dev::step_grid_blocks(e->device, false, false);
+    e->grid = e->use_dyn ? fsb_dev::step_dyn_blocks(e->device)
+                         : fsb_dev::step_grid_blocks(e->device, false, e->use_bulk);
+    e->grid_explicit = e->use_dyn ? e->grid : fsb_dev::step_grid_blocks(e->device, true, false);
     e->grid_coop = fsb_dev::grid_kernel_blocks(e->device);
     e->grid_auto = e->grid;
     int maxgrid = e->grid > e->grid_explicit ? e->grid : e->grid_explicit;
+    if (e->grid_aux > maxgrid) maxgrid = e->grid_aux;
     if (e->grid_coop > maxgrid) maxgrid = e->grid_coop;
     if (2 * e->grid_coop > maxgrid) maxgrid = 2 * e->grid_coop;  // grid kernel: two slot sets
     e->block_cap = maxgrid;
@@ -815,7 +828,7 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     a.world = e->world;
     a.px = px_of(e, nullptr, e->xseq, 0);
     a.trace_out = e->d_scalar;
-    CU(fsb_dev::launch_eat(a, e->grid, e->stream));
+    CU(fsb_dev::launch_eat(a, e->grid_aux, e->stream));
     CU(cudaEventRecord(e->ev1, e->stream));
     double m = 0.0;
     CU(cudaMemcpyAsync(&m, e->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
@@ -1004,7 +1017,7 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
         ea.part_in = all_part(e, (int)((num_steps - 1) & 1));
         ea.world = e->world;
         ea.px = px_of(e, nullptr, x0 + num_steps, 0);
-        CU(fsb_dev::launch_eat(ea, e->grid, e->stream));
+        CU(fsb_dev::launch_eat(ea, e->grid_aux, e->stream));
         e->cur_buf = (int)((num_steps - 1) & 1);
         e->max_valid = e->sums_valid = true;
         e->xseq = x0 + num_steps;
@@ -1038,7 +1051,8 @@ int fsb_engine_set_grid(fsb_engine* e, int ctas) {
 int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta) {
     if (!e) return fail(FSB_ERR_INVALID_ARGUMENT, "null engine");
     if (ctas) *ctas = e->grid;
-    if (threads_per_cta) *threads_per_cta = e->use_bulk ? fsb_dev::kBulkThreads : fsb_dev::kStepThreads;
+    if (threads_per_cta)
+        *threads_per_cta = e->use_bulk ? fsb_dev::kBulkThreads : e->use_dyn ? fsb_dev::kDynThreads : fsb_dev::kStepThreads;
     return FSB_OK;
 }
 

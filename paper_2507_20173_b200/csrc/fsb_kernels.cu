@@ -153,10 +153,6 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -202,11 +198,11 @@ __device__ __forceinline__ Partial wait_and_combine_peers(const PeerXchg& px, in
 // CTA partial -> global; the last CTA to arrive combines all CTA partials in
 // index order and publishes this rank's partial (and, with a peer exchange,
 // pushes it to every rank).
-__device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs& ws, Partial* part_out,
-                                            const PeerXchg& px, int world) {
+// grid_publish: the CTA total `blk` (valid in thread 0) joins the grid reduction.
+__device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs& ws, Partial* part_out,
+                                             const PeerXchg& px, int world) {
     __shared__ Partial scratch[32];
     __shared__ bool am_last;
-    const Partial blk = block_reduce(local, scratch);
     if (threadIdx.x == 0) {
         store_partial(&ws.block_part[blockIdx.x], blk);
         __threadfence();
@@ -226,6 +222,13 @@ __device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs
     }
     const uint64_t epoch = px.peers ? epoch_of(px, px.out_add) : 0ull;
     if (epoch && threadIdx.x < 32) push_to_peers(px, world, epoch, tot);
+}
+
+__device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs& ws, Partial* part_out,
+                                            const PeerXchg& px, int world) {
+    __shared__ Partial scratch[32];
+    const Partial blk = block_reduce(local, scratch);
+    grid_publish(blk, ws, part_out, px, world);
 }
 
 // Programmatic Dependent Launch: block until the predecessor grid has completed
@@ -488,6 +491,119 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(cons
 }
 
 // ---------------------------------------------------------------------------
+// step_kernel_dyn: the same fused pass, one 1024-thread CTA per SM, with the
+// CTA's chunk cut into at most kDynTiles tiles that its warps CLAIM from a
+// shared-memory counter.  With several CTAs per SM the oldest ones win the
+// warp scheduler and the last CTA finishes alone at low occupancy (a 90-120 us
+// spread across CTAs of one step at 1e7 fish, profiles/r03_grid_ctas.jsonl);
+// claiming keeps every warp busy until the chunk is done.  Each tile's partial
+// is accumulated in a fixed order by whichever warp takes it and stored in its
+// own slot, and the slots are folded in tile order, so the sums stay
+// deterministic.  Odd steps claim tiles from the end (L2 reuse, as in step_chunk).
+template <bool kExplicitCur, bool kSane>
+__global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs a) {
+    __shared__ Partial tile_part[kDynTiles];
+    // tile bookkeeping lives in shared memory, not in registers: the hot loop
+    // is at the 64-register limit of 1024-thread CTAs
+    __shared__ unsigned next_tile, s_glo, s_ghi, s_gpt, s_ntiles;
+    const StepParams P = params_of(a.k);
+    pdl_wait_and_release();
+    const Partial prev = combine_prev(a.part_in, a.world, a.px);
+    publish_prev(prev, a.trace_out, a.bary_out);
+    const bool eat = prev.best > 0.0;  // sim.hpp:115
+    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
+    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
+    const uint64_t n = a.n;
+    const uint64_t npairs = n >> 1;
+    const bool rev = a.alternate && (step & 1ull);
+
+    // balanced contiguous chunk of 32-pair groups (32-bit group indices: up
+    // to 2^37 fish per shard); tiles of gpt groups
+    const uint64_t ngroups_all = (npairs + 31) / 32;
+    const unsigned g_lo = (unsigned)(ngroups_all * blockIdx.x / gridDim.x);
+    const unsigned g_hi = (unsigned)(ngroups_all * (blockIdx.x + 1) / gridDim.x);
+    const unsigned ngroups = g_hi - g_lo;
+    const unsigned gpt = (ngroups + kDynTiles - 1) / kDynTiles;
+    if (threadIdx.x == 0) {
+        next_tile = 0;
+        s_glo = g_lo;
+        s_ghi = g_hi;
+        s_gpt = gpt;
+        s_ntiles = gpt ? (ngroups + gpt - 1) / gpt : 0u;
+    }
+    __syncthreads();
+
+    double2* X2 = reinterpret_cast<double2*>(a.s.x);
+    double2* Y2 = reinterpret_cast<double2*>(a.s.y);
+    double2* W2 = reinterpret_cast<double2*>(a.s.w);
+    double2* P2 = reinterpret_cast<double2*>(a.s.p);
+    const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
+    const SoA2 src{X2, Y2, W2, P2, C2};
+    const unsigned lane = threadIdx.x & 31;
+    // one loop over groups; a warp claims its next tile when the current one
+    // is exhausted (warp-uniform branch), flushing the finished tile's partial
+    unsigned grp = 0, gend = 0, tile = ~0u;
+    Partial acc = identity();
+    for (;;) {
+        if (grp == gend) {
+            if (tile != ~0u) {
+                const Partial tp = warp_reduce(acc);
+                if (lane == 0) tile_part[tile] = tp;
+                acc = identity();
+            }
+            unsigned claim = 0;
+            if (lane == 0) claim = atomicAdd(&next_tile, 1u);
+            claim = __shfl_sync(0xffffffffu, claim, 0);
+            const unsigned nt = *(volatile unsigned*)&s_ntiles;
+            if (claim >= nt) break;
+            tile = rev ? nt - 1 - claim : claim;
+            const unsigned gpt_ = *(volatile unsigned*)&s_gpt;
+            const unsigned gh = *(volatile unsigned*)&s_ghi;
+            grp = *(volatile unsigned*)&s_glo + tile * gpt_;
+            gend = (grp + gpt_ < gh) ? grp + gpt_ : gh;
+        }
+        const uint64_t q = (uint64_t)grp * 32 + lane;
+        double2 X[1], Y[1], W[1], Q[1], C[1];
+        const bool valid[1] = {q < npairs};
+        const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
+        if (valid[0]) {
+            X[0] = X2[q];
+            Y[0] = Y2[q];
+            W[0] = W2[q];
+            Q[0] = P2[q];
+            if (kExplicitCur) C[0] = C2[q];
+        }
+        fused_pairs<kExplicitCur, 1, kSane>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
+        if (valid[0]) {
+            X2[q] = X[0];
+            Y2[q] = Y[0];
+            W2[q] = W[0];
+            P2[q] = Q[0];
+        }
+        ++grp;
+    }
+    __syncthreads();
+    Partial cta = identity();
+    if (threadIdx.x < 32) {
+        for (unsigned i = lane; i < s_ntiles; i += 32) fold(cta, tile_part[i]);
+        cta = warp_reduce(cta);
+        if ((n & 1ull) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail fish
+            const uint64_t i = n - 1;
+            double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];
+            const double c = kExplicitCur ? a.s.c[i] : objective(x, y, P.half_pond);
+            Partial tail = identity();
+            fused_fish(x, y, w, p, c, eat, M, a.gfirst + i, step, P, tail);
+            a.s.x[i] = x;
+            a.s.y[i] = y;
+            a.s.w[i] = w;
+            a.s.p[i] = p;
+            fold(cta, tail);
+        }
+    }
+    grid_publish(cta, a.ws, a.part_out, a.px, a.world);
+}
+
+// ---------------------------------------------------------------------------
 // grid_kernel: all T steps in ONE cooperative launch for mid-size schools
 // (the state stays in L2 between steps; no per-step launch).  Each step is
 // step_chunk on every CTA, then a grid barrier that is also the reduction:
@@ -502,6 +618,10 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
     __shared__ Partial scratch[32];
     __shared__ Partial shared_prev;
     Partial prev = identity();  // no pending eat at the start of a run
+#if FSB_GRID_TIMING
+    unsigned long long ts_prev = 0;
+    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_prev));
+#endif
     for (uint64_t k = 0; k < g.num_steps; ++k) {
         const uint64_t step = g.first_step + k;
         const bool eat = prev.best > 0.0;
@@ -512,6 +632,15 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
 #if FSB_GRID_TIMING
         unsigned long long ts0 = 0, ts1 = 0;
         if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
+#if FSB_GRID_TIMING == 2
+        // experiment: every CTA's chunk time of the last step and its SM
+        if (threadIdx.x == 0 && k + 1 == g.num_steps && blockIdx.x < g.num_steps) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g.trace[blockIdx.x] = (double)(ts0 - ts_prev);
+            if (g.bary) g.bary[blockIdx.x] = (double)smid;
+        }
+#endif
 #endif
         // Grid exchange: publish the CTA partial into slot [k&1][b], arrive on
         // the monotonic counter, wait for all G arrivals of this step, then
@@ -538,27 +667,28 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
             shared_prev = tot;
             if (blockIdx.x == 0) {
                 g.trace[k] = tot.best;
-#if FSB_GRID_TIMING
-                // experiment: CTA 0's globaltimer after its chunk, after the
-                // barrier and after the fold, in place of the barycentre sums
-                unsigned long long ts2;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2));
                 if (g.bary) {
+#if FSB_GRID_TIMING == 1
+                    // experiment: CTA 0's globaltimer after its chunk, after the
+                    // barrier and after the fold, in place of the barycentre sums
+                    unsigned long long ts2;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2));
                     g.bary[3 * k + 0] = __longlong_as_double((long long)ts0);
                     g.bary[3 * k + 1] = __longlong_as_double((long long)ts1);
                     g.bary[3 * k + 2] = __longlong_as_double((long long)ts2);
-                }
-#else
-                if (g.bary) {
+#elif FSB_GRID_TIMING == 0
                     g.bary[3 * k + 0] = tot.sx;
                     g.bary[3 * k + 1] = tot.sy;
                     g.bary[3 * k + 2] = tot.sf;
-                }
 #endif
+                }
             }
         }
         __syncthreads();
         prev = shared_prev;
+#if FSB_GRID_TIMING
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_prev));
+#endif
         __syncthreads();  // shared_prev / scratch reuse by the next step
     }
     // trailing eat of the last step, on the fish this CTA itself updated
@@ -1064,6 +1194,19 @@ int grid_for(uint64_t work_items, int device, int per_sm) {
 
 }  // namespace
 
+int step_dyn_blocks(int device) {
+    int per_sm = 0, per_sm_x = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, step_kernel_dyn<false, false>, kDynThreads, 0) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_x, step_kernel_dyn<true, false>, kDynThreads, 0) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        per_sm = per_sm_x = 1;
+    }
+    if (per_sm_x < per_sm) per_sm = per_sm_x;
+    return num_sms(device) * (per_sm < 1 ? 1 : per_sm);
+}
+
 int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
     int per_sm = 0;
     cudaError_t e;
@@ -1112,6 +1255,13 @@ cudaError_t launch_maybe_pdl(void (*kern)(Args), int grid, int block, size_t sme
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
     const bool pdl = a.pdl != 0;
     const bool sane = a.sane != 0;
+    if (a.dyn && !a.bulk) {
+        if (a.s.c)
+            return launch_maybe_pdl(sane ? step_kernel_dyn<true, true> : step_kernel_dyn<true, false>, grid,
+                                    kDynThreads, 0, st, a, pdl);
+        return launch_maybe_pdl(sane ? step_kernel_dyn<false, true> : step_kernel_dyn<false, false>, grid,
+                                kDynThreads, 0, st, a, pdl);
+    }
     if (a.s.c)
         return launch_maybe_pdl(sane ? step_kernel<true, true> : step_kernel<true, false>, grid, kStepThreads, 0, st,
                                 a, pdl);

@@ -58,6 +58,10 @@ constexpr int kThreads = 256;     // threads per CTA of the streaming kernels
 constexpr int kStepThreads = FSB_STEP_THREADS;  // ... of the LDG step kernel and the grid kernel
 constexpr int kPairsPerThread = FSB_PAIRS;  // double2 loads per array per thread per tile
 constexpr int kTilePairs = kStepThreads * kPairsPerThread;
+
+// step_kernel_dyn: one CTA per SM, warps claim tiles of its chunk.
+constexpr int kDynThreads = 1024;
+constexpr int kDynTiles = 1024;   // tile-partial slots per CTA (32 KB of shared memory)
 constexpr int kTileFish = 2 * kTilePairs;
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,
@@ -142,6 +146,7 @@ struct StepArgs {
     int pdl;              // launched as a programmatic dependent of the previous step
     PeerXchg px;          // peer exchange instead of part_in/part_out (px.peers != nullptr)
     int sane;             // state and config in range: guards elided (fsb_math.cuh "In-range mode")
+    int dyn;              // compact LDG path: step_kernel_dyn (one CTA per SM, claimed tiles)
 };
 
 // Persistent cooperative-grid run (FSB_STRATEGY_GRID): `base` supplies the
@@ -199,6 +204,7 @@ struct ClusterArgs {
 };
 
 int step_grid_blocks(int device, bool explicit_cur, bool bulk);
+int step_dyn_blocks(int device);
 cudaError_t launch_init(const InitArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st);

@@ -90,15 +90,19 @@ def test_sizes_bit_exact(orc, n, t, strategy, alternate):
     assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
 
 
+KERNELS = {"static": dict(static_tiles=True), "dynamic": dict(dynamic_tiles=True), "bulk": dict(bulk=True)}
+
+
 @pytest.mark.parametrize("n,t", [(1, 5), (513, 5), (70_001, 6), (1_000_000, 4), (3_000_001, 3)])
 @pytest.mark.parametrize("alternate", [True, False])
-@pytest.mark.parametrize("bulk", [False, "force"])
-def test_step_kernel_variants_bit_exact(orc, n, t, alternate, bulk):
-    """Both compact-state step kernels at every size: the LDG kernel
-    (FSB_FLAG_NO_BULK) and the cp.async.bulk ring (FSB_FLAG_FORCE_BULK)."""
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_step_kernel_variants_bit_exact(orc, n, t, alternate, kernel):
+    """Every compact-state step kernel at every size: the static-chunk LDG
+    kernel, the claimed-tile LDG kernel (FSB_FLAG_DYNAMIC_TILES) and the
+    cp.async.bulk ring (FSB_FLAG_FORCE_BULK)."""
     cfg = fsb.baseline_config(n, t)
     want_fish, want_trace = orc.simulate(ocfg(cfg))
-    with make(cfg, "stream", alternate=alternate, bulk=bulk) as eng:
+    with make(cfg, "stream", alternate=alternate, **KERNELS[kernel]) as eng:
         trace, bary, _ = eng.simulate(barycentre=True)
         got = eng.download()
     assert got.tobytes() == want_fish.tobytes()
@@ -236,16 +240,16 @@ def test_upload_inconsistent_then_run(orc, strategy):
 
 
 @pytest.mark.parametrize("strategy", ["stream", "grid"])
-@pytest.mark.parametrize("bulk", [False, "force"])
+@pytest.mark.parametrize("kernel", list(KERNELS))
 @pytest.mark.parametrize("n,t", [(4097, 9), (300_001, 5)])
-def test_in_range_mode_equals_checked(orc, strategy, bulk, n, t):
+def test_in_range_mode_equals_checked(orc, strategy, kernel, n, t):
     """The step kernels with the fp64 operand guards elided (in-range mode, the
     default for an init'd school) and evaluated (FSB_FLAG_CHECKED) agree with
     the oracle bit for bit."""
     cfg = fsb.baseline_config(n, t)
     want_fish, want_trace = orc.simulate(ocfg(cfg))
     for checked in (False, True):
-        with make(cfg, strategy, bulk=bulk, checked=checked) as eng:
+        with make(cfg, strategy, checked=checked, **KERNELS[kernel]) as eng:
             trace, _, _ = eng.simulate(barycentre=False)
             assert trace.tobytes() == want_trace.tobytes(), checked
             assert eng.download().tobytes() == want_fish.tobytes(), checked
@@ -312,13 +316,13 @@ def test_config_outside_in_range_bounds(orc, over):
         assert eng.download().tobytes() == want_fish.tobytes()
 
 
-@pytest.mark.parametrize("bulk", [False, "force"])
-def test_grid_override_bit_exact(orc, bulk):
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_grid_override_bit_exact(orc, kernel):
     """fsb_engine_set_grid (the CTA-count sweep): any grid, including more CTAs
     than 64-pair blocks, gives the oracle's state and trace."""
     cfg = fsb.baseline_config(100_003, 6)
     want_fish, want_trace = orc.simulate(ocfg(cfg))
-    with make(cfg, "stream", bulk=bulk) as eng:
+    with make(cfg, "stream", **KERNELS[kernel]) as eng:
         auto = eng.grid()
         for ctas in (1, 7, 148, 1000, 5000, 0):
             eng.set_grid(ctas)
@@ -328,6 +332,31 @@ def test_grid_override_bit_exact(orc, bulk):
             assert eng.download().tobytes() == want_fish.tobytes(), ctas
         with pytest.raises(fsb.FsbError):
             eng.set_grid(-1)
+
+
+def test_dynamic_tiles_explicit_cur_and_repeatable(orc):
+    """The claimed-tile kernel on its explicit-cur instantiation (first step
+    after an inconsistent upload), and bitwise repeatability of its sums
+    (tile partials folded in tile order, whichever warp claimed them)."""
+    rng = np.random.default_rng(9)
+    n = 200_003
+    fish = np.zeros(n, dtype=oracle.FISH_DTYPE)
+    fish["x"] = rng.uniform(0, 200, n)
+    fish["y"] = rng.uniform(0, 200, n)
+    fish["weight"] = rng.uniform(1, 2, n)
+    fish["prev_objective"] = rng.uniform(0, 150, n)
+    fish["current_objective"] = rng.uniform(0, 150, n)
+    cfg = fsb.SimConfig(num_fish=n, num_steps=6, seed=41, weight_scale=1.0, pond_size=200.0, step_base=0.1)
+    outs = []
+    for _ in range(2):
+        with make(cfg, "stream", dynamic_tiles=True) as eng:
+            eng.upload(fish)
+            want = fish.copy()
+            trace, bary, _ = eng.run(0, 6, barycentre=True)
+            assert trace.tobytes() == orc.run(ocfg(cfg), want, 0, 6).tobytes()
+            assert eng.download().tobytes() == want.tobytes()
+            outs.append(bary.tobytes())
+    assert outs[0] == outs[1]
 
 
 def test_long_stream_run_is_chunked(orc):

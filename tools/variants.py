@@ -37,6 +37,7 @@ VARIANTS = {
     "t1024b1": ["-DFSB_STEP_THREADS=1024", "-DFSB_MIN_BLOCKS=1"],
     # experiment: grid kernel phase timestamps (tools/grid_phases.py)
     "gridtiming": ["-DFSB_GRID_TIMING=1"],
+    "gridcta": ["-DFSB_GRID_TIMING=2"],
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
