@@ -282,6 +282,7 @@ fsb_dev::StepArgs step_args(fsb_engine* e, const fsb_dev::SoA& s) {
     a.world = e->world;
     a.ws.block_part = e->block_part;
     a.ws.counter = e->counter;
+    a.ws.cap = (unsigned)e->block_cap;
     a.alternate = (e->flags & FSB_FLAG_NO_ALTERNATE) ? 0 : 1;
     a.bulk = e->use_bulk ? 1 : 0;
     a.dyn = e->use_dyn ? 1 : 0;
@@ -464,6 +465,7 @@ int reduce_current(fsb_engine* e) {
     a.n = e->count;
     a.ws.block_part = e->block_part;
     a.ws.counter = e->counter;
+    a.ws.cap = (unsigned)e->block_cap;
     a.part_out = local_part(e, 0);
     a.world = e->world;
     a.px = px_of(e, nullptr, 0, e->xseq + 1);

@@ -162,6 +162,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
 // Peer exchange, producer side (warp 0 of the last CTA): the rank partial into
 // every peer's window, then the epoch flag with release semantics.
 __device__ __forceinline__ void push_to_peers(const PeerXchg& px, int world, uint64_t epoch, const Partial& tot) {
+    FSB_CHECK(world <= kMaxRanks && px.rank >= 0 && px.rank < world);
     const int b = (int)(epoch & 1);
     for (int q = threadIdx.x; q < world; q += 32) {
         PeerWindow* w = px.peers[q];
@@ -204,6 +205,7 @@ __device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs&
     __shared__ Partial scratch[32];
     __shared__ bool am_last;
     if (threadIdx.x == 0) {
+        FSB_CHECK(blockIdx.x < ws.cap);
         store_partial(&ws.block_part[blockIdx.x], blk);
         __threadfence();
         const unsigned prev = atomicAdd(ws.counter, 1u);
@@ -421,6 +423,7 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
     uint64_t hi = (nblk * (blockIdx.x + 1) / gridDim.x) * kAlign;
     if (hi > npairs) hi = npairs;
     const uint64_t nsub = hi > lo ? (hi - lo + kTilePairs - 1) / kTilePairs : 0;
+    FSB_CHECK(lo <= npairs || nsub == 0);
 
     double2* X2 = reinterpret_cast<double2*>(a.s.x);
     double2* Y2 = reinterpret_cast<double2*>(a.s.y);
@@ -557,6 +560,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs
             const unsigned nt = *(volatile unsigned*)&s_ntiles;
             if (claim >= nt) break;
             tile = rev ? nt - 1 - claim : claim;
+            FSB_CHECK(nt <= (unsigned)kDynTiles && tile < nt);
             const unsigned gpt_ = *(volatile unsigned*)&s_gpt;
             const unsigned gh = *(volatile unsigned*)&s_ghi;
             grp = *(volatile unsigned*)&s_glo + tile * gpt_;
@@ -650,6 +654,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
         // only after every CTA has arrived at step k+1, i.e. finished reading.
         Partial* slots = a.ws.block_part + (k & 1) * gridDim.x;
         if (threadIdx.x == 0) {
+            FSB_CHECK(2 * gridDim.x <= a.ws.cap);
             store_partial(&slots[blockIdx.x], blk);
             __threadfence();
             atomicAdd(g.gen, 1ull);
@@ -828,6 +833,7 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
                 const uint64_t base = sub_base(j);
                 const uint64_t cnt = (hi - base < (uint64_t)kBulkTilePairs) ? hi - base : (uint64_t)kBulkTilePairs;
                 const unsigned bytes = (unsigned)(cnt * sizeof(double2));
+                FSB_CHECK(base >= lo && cnt >= 1 && cnt <= (uint64_t)kBulkTilePairs);
                 mbar_expect_tx(&full[s], 4 * bytes);
                 bulk_load(stage[s].x, X2 + mem(base), bytes, &full[s]);
                 bulk_load(stage[s].y, Y2 + mem(base), bytes, &full[s]);

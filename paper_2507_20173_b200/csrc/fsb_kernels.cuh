@@ -14,6 +14,28 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Debug builds (tools/variants.py "debug"): device-side bounds checks that trap
+// with a message -- the substitute for compute-sanitizer, which this GPU pool
+// does not offer.  Compiled out otherwise.
+#ifndef FSB_DEBUG_CHECKS
+#define FSB_DEBUG_CHECKS 0
+#endif
+#if FSB_DEBUG_CHECKS
+#include <cstdio>
+#define FSB_CHECK(c)                                                                   \
+    do {                                                                               \
+        if (!(c)) {                                                                    \
+            printf("FSB_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                             \
+            __trap();                                                                  \
+        }                                                                              \
+    } while (0)
+#else
+#define FSB_CHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 namespace fsb_dev {
 
 // Tuning knobs (compile-time; tools/variants.py builds alternatives for A/B runs).
@@ -101,8 +123,9 @@ struct Scalars {
 
 // Reduction workspace of one launch.
 struct ReduceWs {
-    Partial* block_part;  // [grid]
+    Partial* block_part;  // [cap] (>= grid; the grid kernel uses 2 x grid)
     unsigned* counter;    // zero between launches
+    unsigned cap;         // capacity of block_part (checked by FSB_DEBUG_CHECKS builds)
 };
 
 // Peer exchange (FSB_FLAG_PEER_EXCHANGE): every rank owns one window in its

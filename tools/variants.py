@@ -23,6 +23,8 @@ OUT = os.path.join(ROOT, "build", "variants")
 VARIANTS = {
     # LDG kernel: p<pairs per thread>b<min blocks>; bulk kernel: b<pairs>s<stages>m<min blocks>
     "default": [],
+    # device-side bounds checks (FSB_CHECK) compiled in: run the GPU tests with FSB_LIB pointing here
+    "debug": ["-DFSB_DEBUG_CHECKS=1"],
     "p4b2": ["-DFSB_PAIRS=4", "-DFSB_MIN_BLOCKS=2"],
     "p1b4": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=4"],
     "p2b3": ["-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=3"],
