@@ -68,11 +68,13 @@ typedef struct fsb_timing {
 
 /* Step-loop strategies. */
 enum fsb_strategy {
-    FSB_STRATEGY_AUTO = 0,       /* persistent for small single-GPU schools, else stream */
+    FSB_STRATEGY_AUTO = 0,       /* single GPU: persistent cluster up to 16384 fish, grid up to 2.5e6,
+                                    else stream */
     FSB_STRATEGY_STREAM = 1,     /* one fused step kernel per step, CUDA-graph replayed  */
     FSB_STRATEGY_PERSISTENT = 2, /* one thread-block cluster runs all steps on chip       */
-    FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps,
-                                    a grid barrier per step (single GPU, mid-size schools) */
+    FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps; CTAs
+                                    reduce inside thread-block clusters, clusters meet through one
+                                    flag each (single GPU, mid-size schools) */
 };
 
 /* Engine flags. */
@@ -87,6 +89,7 @@ enum fsb_strategy {
 #define FSB_FLAG_STATIC_TILES 0x80u  /* LDG step kernel: one static chunk per 256-thread CTA, 4 CTAs per SM */
 #define FSB_FLAG_DYNAMIC_TILES 0x100u /* LDG step kernel: one 1024-thread CTA per SM whose warps claim tiles
                                         (default: dynamic from 2e7 fish per shard) */
+#define FSB_FLAG_FLAT_GRID 0x200u   /* FSB_STRATEGY_GRID without thread-block clusters (one counter barrier) */
 #define FSB_FLAG_CHECKED 0x40u     /* always evaluate the fp64 fast-path operand guards (default: elided
                                       while config and state are provably in range; results identical) */
 

@@ -33,6 +33,7 @@ FLAG_PEER_EXCHANGE = 0x20
 FLAG_CHECKED = 0x40
 FLAG_STATIC_TILES = 0x80
 FLAG_DYNAMIC_TILES = 0x100
+FLAG_FLAT_GRID = 0x200
 
 
 class fsb_sim_config(ctypes.Structure):

@@ -157,6 +157,9 @@ struct fsb_engine {
     bool use_dyn = false;    // compact LDG step: step_kernel_dyn (one CTA per SM, claimed tiles)
     int grid_coop = 0;       // grid of the cooperative persistent grid kernel
     unsigned long long* d_gen = nullptr;     // grid-kernel arrival counter
+    int cgrid_nc = 0;                        // co-resident clusters of the cluster-reduced grid kernel (0: none)
+    Partial* d_cl_part = nullptr;            // [2][cgrid_nc]
+    unsigned long long* d_cl_flag = nullptr; // [cgrid_nc]
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
 
     void* staging = nullptr;  // device AoS staging
@@ -252,6 +255,19 @@ bool want_persistent(const fsb_engine* e) {
     if (e->strategy == FSB_STRATEGY_PERSISTENT) return true;
     if (e->strategy == FSB_STRATEGY_STREAM) return false;
     return e->count > 0 && e->count <= 16384;
+}
+
+// FSB_STRATEGY_GRID, and AUTO for mid-size single-rank schools: the
+// cluster-reduced persistent grid kernel measured 3-13% faster than the graph
+// of step kernels from 2e4 to 2e6 fish and slower from 3e6
+// (profiles/r03_ab_grid.jsonl).
+constexpr uint64_t kGridAutoMaxFish = 2500000;
+
+bool want_grid(const fsb_engine* e) {
+    if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode) return false;
+    if (e->strategy == FSB_STRATEGY_GRID) return true;
+    return e->strategy == FSB_STRATEGY_AUTO && e->cgrid_nc > 0 && e->count > 16384 && e->count <= kGridAutoMaxFish &&
+           !(e->flags & (FSB_FLAG_FORCE_BULK | FSB_FLAG_DYNAMIC_TILES | FSB_FLAG_STATIC_TILES));
 }
 
 void free_graphs(fsb_engine* e) {
@@ -397,17 +413,34 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
     if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode)
         return fail(FSB_ERR_UNSUPPORTED, "grid strategy: single rank, compact state only");
     TRY(ensure_run_buffers(e, T));
-    fsb_dev::GridArgs g{};
-    g.base = step_args(e, canonical(e));
-    g.base.part_out = local_part(e, 0);
-    g.first_step = first_step;
-    g.num_steps = T;
-    g.trace = e->d_cl_trace;
-    g.bary = bary ? e->d_cl_bary : nullptr;
-    g.gen = e->d_gen;
-    CU(cudaMemsetAsync(e->d_gen, 0, sizeof(unsigned long long), e->stream));
-    CU(cudaEventRecord(e->ev0, e->stream));
-    CU(fsb_dev::launch_grid_run(g, e->grid_coop, e->stream));
+    fsb_dev::StepArgs base = step_args(e, canonical(e));
+    base.part_out = local_part(e, 0);
+    if (e->cgrid_nc > 0) {
+        // clusters of 8 CTAs reduce over DSMEM; one epoch flag per cluster
+        fsb_dev::CGridArgs g{};
+        g.base = base;
+        g.first_step = first_step;
+        g.num_steps = T;
+        g.trace = e->d_cl_trace;
+        g.bary = bary ? e->d_cl_bary : nullptr;
+        g.cl_part = e->d_cl_part;
+        g.cl_flag = e->d_cl_flag;
+        CU(cudaMemsetAsync(e->d_cl_flag, 0, e->cgrid_nc * fsb_dev::kFlagStride * sizeof(unsigned long long),
+                           e->stream));
+        CU(cudaEventRecord(e->ev0, e->stream));
+        CU(fsb_dev::launch_cgrid_run(g, e->cgrid_nc, e->stream));
+    } else {
+        fsb_dev::GridArgs g{};
+        g.base = base;
+        g.first_step = first_step;
+        g.num_steps = T;
+        g.trace = e->d_cl_trace;
+        g.bary = bary ? e->d_cl_bary : nullptr;
+        g.gen = e->d_gen;
+        CU(cudaMemsetAsync(e->d_gen, 0, sizeof(unsigned long long), e->stream));
+        CU(cudaEventRecord(e->ev0, e->stream));
+        CU(fsb_dev::launch_grid_run(g, e->grid_coop, e->stream));
+    }
     CU(cudaEventRecord(e->ev1, e->stream));
     if (trace) CU(cudaMemcpyAsync(trace, e->d_cl_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     if (bary) CU(cudaMemcpyAsync(bary, e->d_cl_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
@@ -594,6 +627,8 @@ int fsb_engine_destroy(fsb_engine* e) {
     if (e->window) cudaFree(e->window);
     if (e->d_peers) cudaFree(e->d_peers);
     if (e->d_gen) cudaFree(e->d_gen);
+    if (e->d_cl_part) cudaFree(e->d_cl_part);
+    if (e->d_cl_flag) cudaFree(e->d_cl_flag);
     for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
                     (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
                     (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
@@ -687,6 +722,11 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     if (2 * e->grid_coop > maxgrid) maxgrid = 2 * e->grid_coop;  // grid kernel: two slot sets
     e->block_cap = maxgrid;
     CB(cudaMalloc(&e->d_gen, sizeof(unsigned long long)));
+    e->cgrid_nc = (e->flags & FSB_FLAG_FLAT_GRID) ? 0 : fsb_dev::cgrid_clusters(e->device);
+    if (e->cgrid_nc > 0) {
+        CB(cudaMalloc(&e->d_cl_part, 2 * e->cgrid_nc * sizeof(Partial)));
+        CB(cudaMalloc(&e->d_cl_flag, e->cgrid_nc * fsb_dev::kFlagStride * sizeof(unsigned long long)));
+    }
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
     CB(cudaMalloc(&e->counter, sizeof(unsigned)));
@@ -878,8 +918,7 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
         e->max_valid = e->sums_valid = true;
         e->cur_buf = 0;
         e->last_launches = 0;
-    } else if (e->strategy == FSB_STRATEGY_GRID && !e->cur_explicit && e->world == 1 && !e->use_nccl &&
-               !e->peer_mode) {
+    } else if (want_grid(e)) {
         // (the first run after an inconsistent upload takes the stream path below)
         TRY(run_grid(e, first_step, num_steps, trace, bary, &secs));
     } else if (want_persistent(e)) {

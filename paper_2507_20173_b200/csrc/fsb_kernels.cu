@@ -153,6 +153,16 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -1179,6 +1189,171 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     cluster.sync();  // no CTA retires while a peer could still address its shared memory
 }
 
+// ---------------------------------------------------------------------------
+// cgrid_kernel: the grid kernel with a two-level exchange.  Per step each CTA
+// block-reduces its chunk, pushes the CTA partial into its cluster leader's
+// shared memory with st.async (DSMEM, completing bytes on the leader's mbarrier),
+// and each cluster's rank-0 CTA folds the C partials, publishes the cluster
+// partial with an epoch flag (release), polls the other clusters' flags
+// (acquire), folds the cluster partials and pushes the step total back into
+// its cluster.  Every tree is fixed by (grid, cluster size), so the sums are
+// deterministic.  All slots are double-buffered by step parity: a CTA reuses a
+// slot set only after every cluster has published the next step, i.e. after
+// every reader of the old contents has finished.
+// Cluster coordinates re-read from special registers where used (volatile):
+// the step loop runs at the 64-register limit, and values held across it
+// would push the accumulators into local memory.
+__device__ __forceinline__ unsigned sreg_cluster_rank() {
+    unsigned v;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(v));
+    return v;
+}
+__device__ __forceinline__ unsigned sreg_cluster_size() {
+    unsigned v;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(v));
+    return v;
+}
+__device__ __forceinline__ unsigned sreg_cluster_id() {
+    unsigned v;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(v));
+    return v;
+}
+__device__ __forceinline__ unsigned sreg_num_clusters() {
+    unsigned v;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(v));
+    return v;
+}
+
+// The leader warp's half of a step's exchange.
+__device__ __forceinline__ void cgrid_leader_exchange(const CGridArgs& g, uint64_t k, Partial (*slots)[kCGridCluster],
+                                                   Partial* tslot, uint64_t* xbar, uint64_t* tbar) {
+    const unsigned b = (unsigned)(k & 1);
+    const unsigned par = (unsigned)((k >> 1) & 1);
+    const unsigned lane = threadIdx.x;
+    const unsigned C = sreg_cluster_size(), cid = sreg_cluster_id(), NC = sreg_num_clusters();
+    mbar_wait_cluster(&xbar[b], par);
+#if FSB_GRID_TIMING == 1 || FSB_GRID_TIMING == 3
+    unsigned long long tsx, tsf;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tsx));
+#endif
+    Partial cpart = identity();
+    for (unsigned r = 0; r < C; ++r) fold(cpart, slots[b][r]);
+    if (lane == 0) {
+        FSB_CHECK(cid < NC);
+        store_partial(&g.cl_part[b * NC + cid], cpart);
+        st_release_gpu(&g.cl_flag[cid * kFlagStride], k + 1);
+    }
+    // relaxed polls, then ONE acquire fence before the partials are read (an
+    // acquire load per poll would invalidate L1 each time)
+    for (unsigned c = lane; c < NC; c += 32)
+        while (ld_relaxed_gpu(&g.cl_flag[c * kFlagStride]) < k + 1) {
+        }
+    __syncwarp();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    Partial t = identity();
+    for (unsigned c = lane; c < NC; c += 32) fold(t, load_cg(&g.cl_part[b * NC + c]));
+    t = warp_reduce(t);
+#if FSB_GRID_TIMING == 1 || FSB_GRID_TIMING == 3
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tsf));
+#endif
+#if FSB_GRID_TIMING == 3
+    // experiment: every leader's cluster-ready and global-done times of the last step
+    if (lane == 0 && k + 1 == g.num_steps && g.bary && 2 * cid + 1 < 3 * g.num_steps) {
+        g.bary[2 * cid + 0] = __longlong_as_double((long long)tsx);
+        g.bary[2 * cid + 1] = __longlong_as_double((long long)tsf);
+    }
+#endif
+    if (lane < C) {
+        const uint32_t dst = cluster_map(smem_u32(&tslot[b]), lane);
+        const uint32_t bar = cluster_map(smem_u32(&tbar[b]), lane);
+        st_async_f64x2(dst, t.best, t.sx, bar);
+        st_async_f64x2(dst + 16, t.sy, t.sf, bar);
+    }
+    if (cid == 0 && lane == 0) {
+        g.trace[k] = t.best;
+        if (g.bary) {
+#if FSB_GRID_TIMING == 1
+            // experiment: leader 0's globaltimer after the cluster wait and after the global fold
+            g.bary[3 * k + 1] = __longlong_as_double((long long)tsx);
+            g.bary[3 * k + 2] = __longlong_as_double((long long)tsf);
+#elif FSB_GRID_TIMING == 0
+            g.bary[3 * k + 0] = t.sx;
+            g.bary[3 * k + 1] = t.sy;
+            g.bary[3 * k + 2] = t.sf;
+#endif
+        }
+    }
+}
+
+template <bool kSane>
+__global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(const CGridArgs g) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const StepArgs& a = g.base;
+    const StepParams P = params_of(a.k);
+    __shared__ __align__(16) Partial slots[2][kCGridCluster];
+    __shared__ __align__(16) Partial tslot[2];
+    __shared__ __align__(8) uint64_t xbar[2], tbar[2];
+    __shared__ Partial scratch[32];
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&xbar[b], 1);
+            mbar_init(&tbar[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();  // every CTA's barriers exist before anyone pushes into them
+
+    double prev_best = -INFINITY;  // no pending eat at the start of a run (only the max is kept live)
+    for (uint64_t k = 0; k < g.num_steps; ++k) {
+        const unsigned b = (unsigned)(k & 1);
+        if (threadIdx.x == 0) {  // may race the incoming pushes: fine
+            if (sreg_cluster_rank() == 0) mbar_expect_tx(&xbar[b], sreg_cluster_size() * (unsigned)sizeof(Partial));
+            mbar_expect_tx(&tbar[b], (unsigned)sizeof(Partial));
+        }
+        const uint64_t step = g.first_step + k;
+        const bool eat = prev_best > 0.0;
+        const SharedDivisor M = make_divisor(eat ? prev_best : 1.0);
+        Partial acc = identity();
+        step_chunk<false, kSane>(a, P, eat, M, step, acc);
+        const Partial blk = block_reduce(acc, scratch);  // every lane of warp 0 holds it
+#if FSB_GRID_TIMING == 1
+        if (blockIdx.x == 0 && threadIdx.x == 0 && g.bary) {  // experiment: CTA 0 after its chunk
+            unsigned long long ts0;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
+            g.bary[3 * k + 0] = __longlong_as_double((long long)ts0);
+        }
+#endif
+        if (threadIdx.x == 0) {  // this CTA's partial into the leader's slot
+            const uint32_t dst = cluster_map(smem_u32(&slots[b][sreg_cluster_rank()]), 0);
+            const uint32_t bar = cluster_map(smem_u32(&xbar[b]), 0);
+            st_async_f64x2(dst, blk.best, blk.sx, bar);
+            st_async_f64x2(dst + 16, blk.sy, blk.sf, bar);
+        }
+        if (threadIdx.x < 32 && sreg_cluster_rank() == 0) cgrid_leader_exchange(g, k, slots, tslot, xbar, tbar);
+        mbar_wait_cluster(&tbar[b], (unsigned)((k >> 1) & 1));
+        prev_best = tslot[b].best;
+        __syncthreads();  // also a scheduling fence: keeps the step loop's registers in bounds
+    }
+    // trailing eat of the last step, on the fish this CTA itself updated
+    if (prev_best > 0.0 && g.num_steps) {
+        const SharedDivisor M = make_divisor(prev_best);
+        const uint64_t npairs = a.n >> 1;
+        constexpr uint64_t kAlign = 64;  // the chunk of step_chunk
+        const uint64_t nblk = (npairs + kAlign - 1) / kAlign;
+        const uint64_t lo = 2 * ((nblk * blockIdx.x / gridDim.x) * kAlign);
+        uint64_t hi = 2 * ((nblk * (blockIdx.x + 1) / gridDim.x) * kAlign);
+        if (hi > 2 * npairs) hi = 2 * npairs;
+        for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
+            a.s.w[i] = eat_weight(a.s.w[i], a.s.p[i], objective(a.s.x[i], a.s.y[i], P.half_pond), M, P.w_max);
+        if ((a.n & 1ull) && blockIdx.x == 0 && threadIdx.x == 0) {
+            const uint64_t i = a.n - 1;
+            a.s.w[i] = eat_weight(a.s.w[i], a.s.p[i], objective(a.s.x[i], a.s.y[i], P.half_pond), M, P.w_max);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && g.num_steps) store_partial(a.part_out, tslot[(g.num_steps - 1) & 1]);
+    cluster.sync();  // no CTA retires while a peer could still address its shared memory
+}
+
 int g_num_sms[64] = {0};
 
 int num_sms(int device) {
@@ -1303,6 +1478,44 @@ cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st) {
                                    : reinterpret_cast<const void*>(grid_kernel<false>);
     return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kStepThreads), args,
                                        0, st);
+}
+
+namespace {
+cudaLaunchConfig_t cgrid_config(int clusters, cudaStream_t st, cudaLaunchAttribute (&at)[2]) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * kCGridCluster);
+    cfg.blockDim = dim3(kStepThreads);
+    cfg.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCGridCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    return cfg;
+}
+}  // namespace
+
+int cgrid_clusters(int device) {
+    (void)device;
+    cudaLaunchAttribute at[2];
+    cudaLaunchConfig_t cfg = cgrid_config(1, nullptr, at);
+    int n0 = 0, n1 = 0;
+    if (cudaOccupancyMaxActiveClusters(&n0, cgrid_kernel<false>, &cfg) != cudaSuccess ||
+        cudaOccupancyMaxActiveClusters(&n1, cgrid_kernel<true>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n0 < n1 ? n0 : n1;
+}
+
+cudaError_t launch_cgrid_run(const CGridArgs& g, int clusters, cudaStream_t st) {
+    cudaLaunchAttribute at[2];
+    const cudaLaunchConfig_t cfg = cgrid_config(clusters, st, at);
+    return g.base.sane ? cudaLaunchKernelEx(&cfg, cgrid_kernel<true>, g)
+                       : cudaLaunchKernelEx(&cfg, cgrid_kernel<false>, g);
 }
 
 cudaError_t launch_reduce(const ReduceArgs& a, int grid, cudaStream_t st) {

@@ -183,6 +183,22 @@ struct GridArgs {
     unsigned long long* gen;    // arrival counter, zero at launch; base.ws.block_part holds 2 x grid slots
 };
 
+// Cluster-reduced persistent run (FSB_STRATEGY_GRID when cluster launch is
+// available): clusters of kCGridCluster CTAs reduce over DSMEM, cluster
+// leaders meet through one epoch flag per cluster.
+constexpr int kCGridCluster = 8;
+constexpr int kFlagStride = 16;  // u64 words between cluster flags: one 128-B line each (no polling storm on a line)
+
+struct CGridArgs {
+    StepArgs base;
+    uint64_t first_step;
+    uint64_t num_steps;
+    double* trace;                // [num_steps]
+    double* bary;                 // [3*num_steps] or nullptr
+    Partial* cl_part;             // [2][clusters] cluster partials by step parity
+    unsigned long long* cl_flag;  // [clusters * kFlagStride] epoch of each cluster's latest partial, zero at launch
+};
+
 struct EatArgs {
     SoA s;
     Scalars k;
@@ -241,6 +257,9 @@ cudaError_t launch_gather(const SoA& s, double half_pond, const uint64_t* idx, u
 
 // Persistent cooperative-grid run; grid = SMs x occupancy of grid_kernel.
 int grid_kernel_blocks(int device);
+// Co-resident clusters of the cluster-reduced grid kernel (0: not available).
+int cgrid_clusters(int device);
+cudaError_t launch_cgrid_run(const CGridArgs& g, int clusters, cudaStream_t st);
 cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st);
 
 // Cluster kernel: returns cudaErrorNotSupported when n does not fit.

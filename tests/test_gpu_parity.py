@@ -359,6 +359,25 @@ def test_dynamic_tiles_explicit_cur_and_repeatable(orc):
     assert outs[0] == outs[1]
 
 
+@pytest.mark.parametrize("flat", [False, True])
+@pytest.mark.parametrize("n,t", [(1, 4), (1025, 7), (100_003, 6), (2_000_001, 3)])
+def test_grid_strategy_both_exchanges(orc, flat, n, t):
+    """FSB_STRATEGY_GRID with the cluster-reduced exchange (default) and the
+    flat counter barrier (FSB_FLAG_FLAT_GRID): trace and state bit-exact, the
+    per-step barycentre within tolerance, and repeatable bit for bit."""
+    cfg = fsb.baseline_config(n, t)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    outs = []
+    for _ in range(2):
+        with make(cfg, "grid", flat_grid=flat) as eng:
+            trace, bary, _ = eng.simulate(barycentre=True)
+            assert trace.tobytes() == want_trace.tobytes()
+            assert eng.download().tobytes() == want_fish.tobytes()
+            assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
+            outs.append(bary.tobytes())
+    assert outs[0] == outs[1]
+
+
 def test_long_stream_run_is_chunked(orc):
     """A run longer than one graph (1024 steps) goes through several graphs."""
     cfg = fsb.baseline_config(20_000, 2500)

@@ -15,6 +15,8 @@ KERNELS = {
     "dyn": dict(dynamic_tiles=True),  # one CTA per SM, warps claim tiles
     "static": dict(static_tiles=True),  # 4 CTAs per SM, one static chunk each
     "auto": dict(),
+    "cgrid": dict(strategy="grid"),               # cooperative persistent, cluster-reduced exchange
+    "flatgrid": dict(strategy="grid", flat_grid=True),
     "bulk": dict(bulk=True),          # cp.async.bulk shared-memory ring
 }
 names = (sys.argv[1] if len(sys.argv) > 1 else "dyn,static,bulk").split(",")
@@ -23,7 +25,7 @@ if len(sys.argv) > 2:
     sizes = [tuple(int(float(v)) for v in item.split(":")) for item in sys.argv[2].split(",")]
 for n, t in sizes:
     cfg = fsb.baseline_config(n, t)
-    engs = {k: fsb.Engine(cfg, strategy="stream", **KERNELS[k]) for k in names}
+    engs = {k: fsb.Engine(cfg, **{"strategy": "stream", **KERNELS[k]}) for k in names}
     for e in engs.values():
         e.init()
         e.run(0, t)

@@ -40,6 +40,7 @@ VARIANTS = {
     # experiment: grid kernel phase timestamps (tools/grid_phases.py)
     "gridtiming": ["-DFSB_GRID_TIMING=1"],
     "gridcta": ["-DFSB_GRID_TIMING=2"],
+    "gridlead": ["-DFSB_GRID_TIMING=3"],
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
