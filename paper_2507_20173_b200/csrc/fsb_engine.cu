@@ -158,8 +158,7 @@ struct fsb_engine {
     int grid_coop = 0;       // grid of the cooperative persistent grid kernel
     unsigned long long* d_gen = nullptr;     // grid-kernel arrival counter
     int cgrid_nc = 0;                        // co-resident clusters of the cluster-reduced grid kernel (0: none)
-    Partial* d_cl_part = nullptr;            // [2][cgrid_nc]
-    unsigned long long* d_cl_flag = nullptr; // [cgrid_nc]
+    double* d_cl_slots = nullptr;            // [kSlotRing][cgrid_nc][kSlotWords]
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
 
     void* staging = nullptr;  // device AoS staging
@@ -409,6 +408,10 @@ int ensure_run_buffers(fsb_engine* e, uint64_t T) {
 
 // FSB_STRATEGY_GRID: one cooperative launch runs all T steps (compact state,
 // single rank), then the trace comes back.
+size_t cl_slot_bytes(const fsb_engine* e) {
+    return (size_t)fsb_dev::kSlotRing * e->cgrid_nc * fsb_dev::kSlotWords * sizeof(double);
+}
+
 int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary, double* seconds) {
     if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode)
         return fail(FSB_ERR_UNSUPPORTED, "grid strategy: single rank, compact state only");
@@ -423,10 +426,8 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
         g.num_steps = T;
         g.trace = e->d_cl_trace;
         g.bary = bary ? e->d_cl_bary : nullptr;
-        g.cl_part = e->d_cl_part;
-        g.cl_flag = e->d_cl_flag;
-        CU(cudaMemsetAsync(e->d_cl_flag, 0, e->cgrid_nc * fsb_dev::kFlagStride * sizeof(unsigned long long),
-                           e->stream));
+        g.cl_slots = e->d_cl_slots;
+        CU(cudaMemsetAsync(e->d_cl_slots, 0xFF, cl_slot_bytes(e), e->stream));  // every word the sentinel
         CU(cudaEventRecord(e->ev0, e->stream));
         CU(fsb_dev::launch_cgrid_run(g, e->cgrid_nc, e->stream));
     } else {
@@ -627,8 +628,7 @@ int fsb_engine_destroy(fsb_engine* e) {
     if (e->window) cudaFree(e->window);
     if (e->d_peers) cudaFree(e->d_peers);
     if (e->d_gen) cudaFree(e->d_gen);
-    if (e->d_cl_part) cudaFree(e->d_cl_part);
-    if (e->d_cl_flag) cudaFree(e->d_cl_flag);
+    if (e->d_cl_slots) cudaFree(e->d_cl_slots);
     for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
                     (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
                     (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
@@ -724,8 +724,7 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     CB(cudaMalloc(&e->d_gen, sizeof(unsigned long long)));
     e->cgrid_nc = (e->flags & FSB_FLAG_FLAT_GRID) ? 0 : fsb_dev::cgrid_clusters(e->device);
     if (e->cgrid_nc > 0) {
-        CB(cudaMalloc(&e->d_cl_part, 2 * e->cgrid_nc * sizeof(Partial)));
-        CB(cudaMalloc(&e->d_cl_flag, e->cgrid_nc * fsb_dev::kFlagStride * sizeof(unsigned long long)));
+        CB(cudaMalloc(&e->d_cl_slots, cl_slot_bytes(e)));
     }
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));

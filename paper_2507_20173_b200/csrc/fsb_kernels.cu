@@ -153,14 +153,14 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
 
-__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ void red_add_release_gpu(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.add.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
@@ -177,8 +177,7 @@ __device__ __forceinline__ void push_to_peers(const PeerXchg& px, int world, uin
     for (int q = threadIdx.x; q < world; q += 32) {
         PeerWindow* w = px.peers[q];
         store_partial(&w->slots[b][px.rank], tot);
-        __threadfence_system();
-        st_release_sys(&w->flags[b][px.rank], epoch);
+        st_release_sys(&w->flags[b][px.rank], epoch);  // orders the slot stores before the flag
     }
 }
 
@@ -217,13 +216,14 @@ __device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs&
     if (threadIdx.x == 0) {
         FSB_CHECK(blockIdx.x < ws.cap);
         store_partial(&ws.block_part[blockIdx.x], blk);
-        __threadfence();
-        const unsigned prev = atomicAdd(ws.counter, 1u);
-        am_last = (prev == gridDim.x - 1);
+        // release: this CTA's partial before its arrival; acquire: the last
+        // arriver sees every partial (the counter's release sequence).  The
+        // other threads of the last CTA are ordered after it by the barrier
+        // and read with ld.cg (L2), so no fence of their own.
+        am_last = (atom_add_acq_rel_gpu(ws.counter, 1u) == gridDim.x - 1);
     }
     __syncthreads();
     if (!am_last) return;
-    __threadfence();
     Partial acc = identity();
     for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) fold(acc, load_cg(&ws.block_part[i]));
     __syncthreads();  // scratch reuse
@@ -666,8 +666,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
         if (threadIdx.x == 0) {
             FSB_CHECK(2 * gridDim.x <= a.ws.cap);
             store_partial(&slots[blockIdx.x], blk);
-            __threadfence();
-            atomicAdd(g.gen, 1ull);
+            red_add_release_gpu(g.gen, 1ull);
             const unsigned long long target = (k + 1) * (unsigned long long)gridDim.x;
             while (ld_acquire_gpu(g.gen) < target) __nanosleep(20);
 #if FSB_GRID_TIMING
@@ -1224,6 +1223,26 @@ __device__ __forceinline__ unsigned sreg_num_clusters() {
     return v;
 }
 
+__device__ __forceinline__ void st_relaxed_f64(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+__device__ __forceinline__ double ld_relaxed_f64(const double* p) {
+    double v;
+    asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ bool is_sentinel(double v) {
+    return static_cast<unsigned long long>(__double_as_longlong(v)) == kSlotSentinel;
+}
+
+// A value equal to the sentinel pattern (a NaN no arithmetic produces) is
+// published as the canonical NaN instead, so a poll can never wait on it.
+__device__ __forceinline__ double slot_value(double v) {
+    return is_sentinel(v) ? __longlong_as_double(0x7fffffffffffffffll) : v;
+}
+
 // The leader warp's half of a step's exchange.
 __device__ __forceinline__ void cgrid_leader_exchange(const CGridArgs& g, uint64_t k, Partial (*slots)[kCGridCluster],
                                                    Partial* tslot, uint64_t* xbar, uint64_t* tbar) {
@@ -1238,20 +1257,43 @@ __device__ __forceinline__ void cgrid_leader_exchange(const CGridArgs& g, uint64
 #endif
     Partial cpart = identity();
     for (unsigned r = 0; r < C; ++r) fold(cpart, slots[b][r]);
+    // Cluster partials travel in self-validating slots: ring position k % 3,
+    // one 128-B line per cluster, every word the SENTINEL until this step's
+    // value lands, so a poll that sees four non-sentinel words has the data --
+    // one round trip, no separate flag.  The publisher first re-arms its slot
+    // of step k-2 (every leader has read it: each published step k-1, which
+    // it does only after reading step k-2), then a release fence, then the
+    // values; readers end with an acquire fence, which makes the re-arm
+    // visible before they poll that slot again at step k+1.
+    double* const ring = g.cl_slots;
     if (lane == 0) {
         FSB_CHECK(cid < NC);
-        store_partial(&g.cl_part[b * NC + cid], cpart);
-        st_release_gpu(&g.cl_flag[cid * kFlagStride], k + 1);
-    }
-    // relaxed polls, then ONE acquire fence before the partials are read (an
-    // acquire load per poll would invalidate L1 each time)
-    for (unsigned c = lane; c < NC; c += 32)
-        while (ld_relaxed_gpu(&g.cl_flag[c * kFlagStride]) < k + 1) {
+        if (k >= 2) {
+            volatile double* old = ring + ((k + 1) % kSlotRing * NC + cid) * kSlotWords;
+            for (int w = 0; w < 4; ++w) old[w] = __longlong_as_double((long long)kSlotSentinel);
         }
-    __syncwarp();
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("fence.release.gpu;" ::: "memory");  // MEMBAR only
+        double* mine = ring + (k % kSlotRing * NC + cid) * kSlotWords;
+        st_relaxed_f64(mine + 0, slot_value(cpart.best));
+        st_relaxed_f64(mine + 1, slot_value(cpart.sx));
+        st_relaxed_f64(mine + 2, slot_value(cpart.sy));
+        st_relaxed_f64(mine + 3, slot_value(cpart.sf));
+    }
     Partial t = identity();
-    for (unsigned c = lane; c < NC; c += 32) fold(t, load_cg(&g.cl_part[b * NC + c]));
+    for (unsigned c = lane; c < NC; c += 32) {
+        const double* src = ring + (k % kSlotRing * NC + c) * kSlotWords;
+        Partial v;
+        for (;;) {
+            v.best = ld_relaxed_f64(src + 0);
+            v.sx = ld_relaxed_f64(src + 1);
+            v.sy = ld_relaxed_f64(src + 2);
+            v.sf = ld_relaxed_f64(src + 3);
+            if (!is_sentinel(v.best) && !is_sentinel(v.sx) && !is_sentinel(v.sy) && !is_sentinel(v.sf)) break;
+        }
+        fold(t, v);
+    }
+    __syncwarp();
+    asm volatile("fence.acquire.gpu;" ::: "memory");  // L1 invalidate only, no MEMBAR
     t = warp_reduce(t);
 #if FSB_GRID_TIMING == 1 || FSB_GRID_TIMING == 3
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tsf));

@@ -187,7 +187,9 @@ struct GridArgs {
 // available): clusters of kCGridCluster CTAs reduce over DSMEM, cluster
 // leaders meet through one epoch flag per cluster.
 constexpr int kCGridCluster = 8;
-constexpr int kFlagStride = 16;  // u64 words between cluster flags: one 128-B line each (no polling storm on a line)
+constexpr int kSlotRing = 3;     // cluster-partial slot sets (step k uses k % 3)
+constexpr int kSlotWords = 16;   // doubles per cluster slot: one 128-B line each (no polling storm on a line)
+constexpr unsigned long long kSlotSentinel = ~0ull;  // "not yet written" (a NaN pattern arithmetic never yields)
 
 struct CGridArgs {
     StepArgs base;
@@ -195,8 +197,7 @@ struct CGridArgs {
     uint64_t num_steps;
     double* trace;                // [num_steps]
     double* bary;                 // [3*num_steps] or nullptr
-    Partial* cl_part;             // [2][clusters] cluster partials by step parity
-    unsigned long long* cl_flag;  // [clusters * kFlagStride] epoch of each cluster's latest partial, zero at launch
+    double* cl_slots;             // [kSlotRing][clusters][kSlotWords], all bytes 0xFF (sentinel) at launch
 };
 
 struct EatArgs {
