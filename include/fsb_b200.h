@@ -73,8 +73,8 @@ enum fsb_strategy {
     FSB_STRATEGY_STREAM = 1,     /* one fused step kernel per step, CUDA-graph replayed  */
     FSB_STRATEGY_PERSISTENT = 2, /* one thread-block cluster runs all steps on chip       */
     FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps; CTAs
-                                    reduce inside thread-block clusters, clusters meet through one
-                                    flag each (single GPU, mid-size schools) */
+                                    reduce inside thread-block clusters, cluster leaders meet through
+                                    one global slot each (single GPU, mid-size schools) */
 };
 
 /* Engine flags. */

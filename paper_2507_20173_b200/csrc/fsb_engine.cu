@@ -419,7 +419,7 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
     fsb_dev::StepArgs base = step_args(e, canonical(e));
     base.part_out = local_part(e, 0);
     if (e->cgrid_nc > 0) {
-        // clusters of 8 CTAs reduce over DSMEM; one epoch flag per cluster
+        // clusters of 8 CTAs reduce over DSMEM; leaders meet through sentinel slots
         fsb_dev::CGridArgs g{};
         g.base = base;
         g.first_step = first_step;

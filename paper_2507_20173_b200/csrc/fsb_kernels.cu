@@ -1193,12 +1193,12 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
 // block-reduces its chunk, pushes the CTA partial into its cluster leader's
 // shared memory with st.async (DSMEM, completing bytes on the leader's mbarrier),
 // and each cluster's rank-0 CTA folds the C partials, publishes the cluster
-// partial with an epoch flag (release), polls the other clusters' flags
-// (acquire), folds the cluster partials and pushes the step total back into
-// its cluster.  Every tree is fixed by (grid, cluster size), so the sums are
-// deterministic.  All slots are double-buffered by step parity: a CTA reuses a
-// slot set only after every cluster has published the next step, i.e. after
-// every reader of the old contents has finished.
+// partial in a self-validating global slot (see cgrid_leader_exchange), polls
+// every cluster's slot, folds the cluster partials and pushes the step total
+// back into its cluster.  Every tree is fixed by (grid, cluster size), so the
+// sums are deterministic.  Shared-memory slots are double-buffered by step
+// parity: a CTA reuses a slot only after every cluster has published the next
+// step, i.e. after every reader of the old contents has finished.
 // Cluster coordinates re-read from special registers where used (volatile):
 // the step loop runs at the 64-register limit, and values held across it
 // would push the accumulators into local memory.

@@ -185,7 +185,7 @@ struct GridArgs {
 
 // Cluster-reduced persistent run (FSB_STRATEGY_GRID when cluster launch is
 // available): clusters of kCGridCluster CTAs reduce over DSMEM, cluster
-// leaders meet through one epoch flag per cluster.
+// leaders meet through self-validating slots (one 128-B line per cluster).
 constexpr int kCGridCluster = 8;
 constexpr int kSlotRing = 3;     // cluster-partial slot sets (step k uses k % 3)
 constexpr int kSlotWords = 16;   // doubles per cluster slot: one 128-B line each (no polling storm on a line)
