@@ -186,7 +186,10 @@ struct GridArgs {
 // Cluster-reduced persistent run (FSB_STRATEGY_GRID when cluster launch is
 // available): clusters of kCGridCluster CTAs reduce over DSMEM, cluster
 // leaders meet through self-validating slots (one 128-B line per cluster).
-constexpr int kCGridCluster = 8;
+#ifndef FSB_CGRID_CLUSTER
+#define FSB_CGRID_CLUSTER 8
+#endif
+constexpr int kCGridCluster = FSB_CGRID_CLUSTER;
 constexpr int kSlotRing = 3;     // cluster-partial slot sets (step k uses k % 3)
 constexpr int kSlotWords = 16;   // doubles per cluster slot: one 128-B line each (no polling storm on a line)
 constexpr unsigned long long kSlotSentinel = ~0ull;  // "not yet written" (a NaN pattern arithmetic never yields)

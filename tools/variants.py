@@ -41,6 +41,9 @@ VARIANTS = {
     "gridtiming": ["-DFSB_GRID_TIMING=1"],
     "gridcta": ["-DFSB_GRID_TIMING=2"],
     "gridlead": ["-DFSB_GRID_TIMING=3"],
+    # cluster-reduced grid kernel: CTAs per cluster
+    "cg2": ["-DFSB_CGRID_CLUSTER=2"],
+    "cg4": ["-DFSB_CGRID_CLUSTER=4"],
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
