@@ -92,6 +92,23 @@ __device__ __forceinline__ Partial block_reduce(Partial v, Partial* scratch) {
 }
 
 // Max-only reductions (the persistent kernel when no barycentre is requested).
+// Exact fp64 max over a warp with two REDUX (u32) steps instead of five
+// shuffle levels: an order-preserving 64-bit key (sign-folded), max of the
+// high words, then max of the low words among the lanes that hold that high
+// word.  NaN maps to the key of -inf, so -- as in the reference's strict '>'
+// fold (executor.hpp:90) -- it never wins.
+__device__ __forceinline__ double warp_max_redux(double v) {
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    if (v != v) b = 0xfff0000000000000ull;  // NaN -> -inf
+    const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(key >> 32));
+    const unsigned lo = __reduce_max_sync(
+        0xffffffffu, static_cast<unsigned>(key >> 32) == hi ? static_cast<unsigned>(key) : 0u);
+    const unsigned long long m = (static_cast<unsigned long long>(hi) << 32) | lo;
+    const unsigned long long bits = (m >> 63) ? (m & 0x7fffffffffffffffull) : ~m;
+    return __longlong_as_double(static_cast<long long>(bits));
+}
+
 __device__ __forceinline__ double warp_reduce_max(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -104,13 +121,13 @@ __device__ __forceinline__ double warp_reduce_max(double v) {
 __device__ __forceinline__ double block_reduce_max(double v, double* scratch) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    v = warp_reduce_max(v);
+    v = warp_max_redux(v);
     if (lane == 0) scratch[warp] = v;
     __syncthreads();
     double r = -INFINITY;
     if (warp == 0) {
         if (lane < (int)(blockDim.x >> 5)) r = scratch[lane];
-        r = warp_reduce_max(r);
+        r = warp_max_redux(r);
     }
     return r;
 }
@@ -1153,13 +1170,12 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
         mbar_wait_cluster(&xbar[b], (unsigned)((k >> 1) & 1));
         tot = identity();
-        if (kBary) {
-            for (unsigned r = 0; r < ncta; ++r) fold(tot, slots[k & 1][r]);
-        } else {
-            for (unsigned r = 0; r < ncta; ++r) {
-                const double v = slots[k & 1][r].best;
-                tot.best = (v > tot.best) ? v : tot.best;
-            }
+        if (kBary) {  // every warp folds the <= 16 CTA partials itself (fixed butterfly)
+            const unsigned lane = threadIdx.x & 31;
+            tot = warp_reduce(lane < ncta ? slots[k & 1][lane] : identity());
+        } else {  // every warp folds the <= 16 CTA maxima itself: one LDS + two REDUX
+            const unsigned lane = threadIdx.x & 31;
+            tot.best = warp_max_redux(lane < ncta ? slots[k & 1][lane].best : -INFINITY);
         }
         M = tot.best;
         if (crank == 0 && threadIdx.x == 0) {
@@ -1255,8 +1271,7 @@ __device__ __forceinline__ void cgrid_leader_exchange(const CGridArgs& g, uint64
     unsigned long long tsx, tsf;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tsx));
 #endif
-    Partial cpart = identity();
-    for (unsigned r = 0; r < C; ++r) fold(cpart, slots[b][r]);
+    const Partial cpart = warp_reduce(lane < C ? slots[b][lane] : identity());  // fixed butterfly
     // Cluster partials travel in self-validating slots: ring position k % 3,
     // one 128-B line per cluster, every word the SENTINEL until this step's
     // value lands, so a poll that sees four non-sentinel words has the data --
