@@ -15,7 +15,7 @@ import paper_2507_20173_b200 as fsb  # noqa: E402
 T = 1000
 for n in (1_000_000, 10_000_000):
     cfg = fsb.baseline_config(n, T)
-    with fsb.Engine(cfg, strategy="grid") as eng:
+    with fsb.Engine(cfg, strategy="grid", flat_grid=True) as eng:
         G = eng.grid()[0]
         eng.init()
         trace, bary, _ = eng.run(0, T, barycentre=True)

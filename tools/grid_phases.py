@@ -1,4 +1,4 @@
-"""Phase timing of the grid kernel's per-step exchange (experiment build
+"""Phase timing of the flat grid kernel (FSB_FLAG_FLAT_GRID)'s per-step exchange (experiment build
 build/variants/libfsb_gridtiming.so): CTA 0's globaltimer after its chunk,
 after the arrival barrier and after the fold, per step.
 
@@ -17,7 +17,7 @@ import paper_2507_20173_b200 as fsb  # noqa: E402
 T = 200
 for n in (2_000, 1_000_000):
     cfg = fsb.baseline_config(n, T)
-    with fsb.Engine(cfg, strategy="grid") as eng:
+    with fsb.Engine(cfg, strategy="grid", flat_grid=True) as eng:
         eng.init()
         eng.run(0, T, barycentre=True)
         eng.init()
