@@ -29,6 +29,8 @@ VARIANTS = {
     "p1b4": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=4"],
     "p2b3": ["-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=3"],
     "p2b2": ["-DFSB_PAIRS=2", "-DFSB_MIN_BLOCKS=2"],
+    "p1b5": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=5"],
+    "p1b6": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=6"],
     "b2s3m2": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=3", "-DFSB_BULK_MIN_BLOCKS=2"],
     "b1s4m3": ["-DFSB_BULK_PAIRS=1", "-DFSB_BULK_STAGES=4", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
