@@ -213,26 +213,29 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def load_profile_traffic(n: int):
-    """dram bytes per step-kernel launch from the committed ncu --set full summary."""
+def load_profile_traffic(n: int, kernel: str):
+    """dram bytes per step-kernel launch from the committed ncu --set full summary
+    (only when it captured the same kernel at the same school size)."""
     path = os.path.join(ROOT, "profiles", "step_kernel_ncu.json")
     try:
         with open(path) as f:
             p = json.load(f)
-        if int(p.get("fish", -1)) == n:
+        if int(p.get("fish", -1)) == n and p.get("kernel_id", "step_kernel") == kernel:
             return float(p["dram_bytes_per_launch"]), p.get("source")
     except Exception:
         pass
     return None, None
 
 
-def issue_roofline(n: int, kernel_s: float, clocks: dict):
+def issue_roofline(n: int, kernel: str, kernel_s: float, clocks: dict):
     """The step kernel's second roofline: SM instruction issue (one warp
     instruction per SMSP per cycle).  Instructions per fish from the committed
     ncu capture (profiles/step_kernel_ncu.json), clock from the timed region."""
     try:
         with open(os.path.join(ROOT, "profiles", "step_kernel_ncu.json")) as f:
             p = json.load(f)
+        if p.get("kernel_id", "step_kernel") != kernel:
+            return None
         instr_per_fish = float(p["thread_instructions_per_fish"])
     except Exception:
         return None
@@ -294,7 +297,9 @@ def run_ours(args, world, rank, local):
     kernel_s = float(np.mean(kms[1:])) * 1e-3 if len(kms) > 1 else float(kms[0]) * 1e-3
     peak_gbs, peak_src = peaks()
     achieved = BYTES_PER_UPDATE * n_local / kernel_s / 1e9
-    traffic, traffic_src = load_profile_traffic(n_local)
+    _, cta_threads = eng.grid()
+    kernel = "step_kernel_dyn" if cta_threads == 1024 else ("step_kernel_bulk" if args.bulk else "step_kernel")
+    traffic, traffic_src = load_profile_traffic(n_local, kernel)
 
     # e2e through the C-ABI with host buffers (pinned), all copies timed
     e2e = None
@@ -358,7 +363,7 @@ def run_ours(args, world, rank, local):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "step_kernel",
+                "kernel": kernel,
                 "achieved": achieved,
                 "peak": peak_gbs,
                 "unit": "GB/s",
@@ -375,7 +380,7 @@ def run_ours(args, world, rank, local):
                 "peak_source": peak_src,
                 "traffic_source": traffic_src,
             },
-            "issue_roofline": issue_roofline(n_local, kernel_s, clk.summary()),
+            "issue_roofline": issue_roofline(n_local, kernel, kernel_s, clk.summary()),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -88,7 +88,7 @@ enum fsb_strategy {
                                         itself (CUDA IPC windows) instead of an NCCL allgather */
 #define FSB_FLAG_STATIC_TILES 0x80u  /* LDG step kernel: one static chunk per 256-thread CTA, 4 CTAs per SM */
 #define FSB_FLAG_DYNAMIC_TILES 0x100u /* LDG step kernel: one 1024-thread CTA per SM whose warps claim tiles
-                                        (default: dynamic from 2e7 fish per shard) */
+                                        (default: dynamic from 3e6 fish per shard) */
 #define FSB_FLAG_FLAT_GRID 0x200u   /* FSB_STRATEGY_GRID without thread-block clusters (one counter barrier) */
 #define FSB_FLAG_CHECKED 0x40u     /* always evaluate the fp64 fast-path operand guards (default: elided
                                       while config and state are provably in range; results identical) */

@@ -106,9 +106,11 @@ int nccl_fail(ncclResult_t r, const char* what) {
 }
 
 constexpr uint64_t kStagingFish = 1ull << 22;  // 160 MB AoS staging per chunk
-// Shards from this size take step_kernel_dyn (3-5% faster from 5e7 fish, even
-// at 1e7-2e7, slower on L2-resident schools: profiles/r03_ab_kernels.jsonl).
-constexpr uint64_t kDynamicMinFish = 20000000;
+// Shards from this size take step_kernel_dyn: with the RNG drawn ahead of the
+// loaded state and tiles of >= 4 groups it is 1-6% faster than the static
+// chunks from 3e6 fish (C1 1e7: 111-114 vs 115-121 us), slower below
+// (profiles/r04_ab_dyn.jsonl).
+constexpr uint64_t kDynamicMinFish = 3000000;
 
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
@@ -189,6 +191,7 @@ fsb_dev::Scalars scalars_of(const fsb_sim_config& c) {
     k.step_base = c.step_base;
     k.w_max = 2.0 * c.weight_scale;  // SimConfig::weight_max (sim.hpp:42)
     k.seed = c.seed;
+    k.zero = 0;
     return k;
 }
 

@@ -300,6 +300,7 @@ __device__ __forceinline__ StepParams params_of(const Scalars& k) {
     P.step_base = k.step_base;
     P.w_max = k.w_max;
     P.seed = k.seed;
+    P.zero = k.zero;
     return P;
 }
 
@@ -359,7 +360,7 @@ struct SoA2 {
 // then are the fish folded into the thread partial.  kSane: the state is in
 // range (fsb_math.cuh "In-range mode"); the eat divisor -- the global max,
 // which other ranks' states feed -- is range-checked here, once per call.
-template <bool kExplicitCur, int U, bool kSane>
+template <bool kExplicitCur, int U, bool kSane, bool kRngFirst = false>
 __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], double2 (&W)[U],
                                             double2 (&Q)[U], const double2 (&C)[U], const bool (&valid)[U],
                                             const SoA2& src, const uint64_t (&k)[U], const uint64_t (&gi)[U],
@@ -371,18 +372,65 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
     // M.b in [2^-506, 2^502] (positive: as an integer range on its bits)
     const uint64_t mb = static_cast<uint64_t>(__double_as_longlong(M.b));
     const bool ok0 = !kSane || !eat || (mb - 0x2050000000000000ull <= 0x3F00000000000000ull);
+    if (kRngFirst) {
+        // Every fish's units first: they depend on (seed, fish, step) only, so the
+        // chains run while the state loads are in flight.  The loaded values then
+        // pass through a fake dependency on the last draws (high word | (bits &
+        // zero), zero == 0 at run time), which keeps ptxas from hoisting their
+        // arithmetic above the chains.  U0/U1 hold the 53-bit integers of the
+        // draws (swim_units_guarded scales them).  Used by the claimed-tile kernel (HBM-latency bound:
+        // C2 2.8% faster); the L2-resident cluster grid runs 22% slower with it.
+        double U0[U][2], U1[U][2];
+        unsigned dep = 0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        ok[u] = ok0;
-        if (valid[u]) {
-            const double c0 =
-                kExplicitCur ? C[u].x : objective_guarded<kSane>(X[u].x, Y[u].x, P.half_pond, ok[u]);
-            const double c1 =
-                kExplicitCur ? C[u].y : objective_guarded<kSane>(X[u].y, Y[u].y, P.half_pond, ok[u]);
-            n0[u] = fused_fish_guarded<kSane>(X[u].x, Y[u].x, W[u].x, Q[u].x, c0, eat, M, gi[u], step, P, ok[u]);
-            n1[u] = fused_fish_guarded<kSane>(X[u].y, Y[u].y, W[u].y, Q[u].y, c1, eat, M, gi[u] + 1, step, P,
-                                              ok[u]);
-            all_ok &= ok[u];
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+                const uint64_t h_step = fold_in(fold_in(P.seed, gi[u] + f), step);
+                const uint64_t b0 = fold_in(h_step, 0);
+                const uint64_t b1 = fold_in(h_step, 1);
+                U0[u][f] = __ull2double_rn(b0 >> 11);
+                U1[u][f] = __ull2double_rn(b1 >> 11);
+                dep |= static_cast<unsigned>(b1);
+            }
+        }
+        dep &= static_cast<unsigned>(P.zero);
+        // the fence goes into high words (one LOP3 each)
+        auto fenced = [dep](double v) {
+            return __hiloint2double(__double2hiint(v) | static_cast<int>(dep), __double2loint(v));
+        };
+        const double hp = fenced(P.half_pond);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ok[u] = ok0;
+            if (valid[u]) {
+                const double c0 = kExplicitCur ? C[u].x : objective_guarded<kSane>(X[u].x, Y[u].x, hp, ok[u]);
+                const double c1 = kExplicitCur ? C[u].y : objective_guarded<kSane>(X[u].y, Y[u].y, hp, ok[u]);
+                double w0 = fenced(W[u].x);
+                double w1 = fenced(W[u].y);
+                if (eat) w0 = eat_weight_guarded<kSane>(w0, Q[u].x, c0, M, P.w_max, ok[u]);
+                if (eat) w1 = eat_weight_guarded<kSane>(w1, Q[u].y, c1, M, P.w_max, ok[u]);
+                W[u] = make_double2(w0, w1);
+                n0[u] = swim_units_guarded<kSane>(X[u].x, Y[u].x, w0, U0[u][0], U1[u][0], P, ok[u]);
+                n1[u] = swim_units_guarded<kSane>(X[u].y, Y[u].y, w1, U0[u][1], U1[u][1], P, ok[u]);
+                Q[u] = make_double2(c0, c1);
+                all_ok &= ok[u];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ok[u] = ok0;
+            if (valid[u]) {
+                const double c0 =
+                    kExplicitCur ? C[u].x : objective_guarded<kSane>(X[u].x, Y[u].x, P.half_pond, ok[u]);
+                const double c1 =
+                    kExplicitCur ? C[u].y : objective_guarded<kSane>(X[u].y, Y[u].y, P.half_pond, ok[u]);
+                n0[u] = fused_fish_guarded<kSane>(X[u].x, Y[u].x, W[u].x, Q[u].x, c0, eat, M, gi[u], step, P, ok[u]);
+                n1[u] = fused_fish_guarded<kSane>(X[u].y, Y[u].y, W[u].y, Q[u].y, c1, eat, M, gi[u] + 1, step, P,
+                                                  ok[u]);
+                all_ok &= ok[u];
+            }
         }
     }
     if (__any_sync(__activemask(), !all_ok)) {  // never taken for in-range simulation values
@@ -553,7 +601,8 @@ __global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs
     const unsigned g_lo = (unsigned)(ngroups_all * blockIdx.x / gridDim.x);
     const unsigned g_hi = (unsigned)(ngroups_all * (blockIdx.x + 1) / gridDim.x);
     const unsigned ngroups = g_hi - g_lo;
-    const unsigned gpt = (ngroups + kDynTiles - 1) / kDynTiles;
+    unsigned gpt = (ngroups + kDynTiles - 1) / kDynTiles;
+    if (gpt < kDynMinGroups) gpt = kDynMinGroups;  // claims + tile flushes amortised over >= kDynMinGroups groups
     if (threadIdx.x == 0) {
         next_tile = 0;
         s_glo = g_lo;
@@ -604,7 +653,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs
             Q[0] = P2[q];
             if (kExplicitCur) C[0] = C2[q];
         }
-        fused_pairs<kExplicitCur, 1, kSane>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
+        fused_pairs<kExplicitCur, 1, kSane, true>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
         if (valid[0]) {
             X2[q] = X[0];
             Y2[q] = Y[0];

@@ -54,7 +54,6 @@ namespace fsb_dev {
 #define FSB_MEM_WINDOW 0
 #endif
 
-
 #ifndef FSB_CLUSTER_MIN_FISH
 #define FSB_CLUSTER_MIN_FISH 256  // persistent kernel: fish per CTA before adding CTAs
 #endif
@@ -84,6 +83,10 @@ constexpr int kTilePairs = kStepThreads * kPairsPerThread;
 // step_kernel_dyn: one CTA per SM, warps claim tiles of its chunk.
 constexpr int kDynThreads = 1024;
 constexpr int kDynTiles = 1024;   // tile-partial slots per CTA (32 KB of shared memory)
+#ifndef FSB_DYN_MIN_GROUPS
+#define FSB_DYN_MIN_GROUPS 4
+#endif
+constexpr unsigned kDynMinGroups = FSB_DYN_MIN_GROUPS;  // minimum 32-pair groups per claimed tile
 constexpr int kTileFish = 2 * kTilePairs;
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,
@@ -119,6 +122,7 @@ struct Scalars {
     double step_base;
     double w_max;
     uint64_t seed;
+    uint64_t zero;  // always 0; opaque to the compiler (the RNG-first scheduling fence)
 };
 
 // Reduction workspace of one launch.

@@ -49,17 +49,23 @@ VARIANTS = {
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
+    # claimed-tile kernel: minimum 32-pair groups per tile
+    "dg1": ["-DFSB_DYN_MIN_GROUPS=1"],
+    "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
+    "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
     # experiment: LDG kernel with all memory folded into 8K pairs (compute-only time)
     "l2_p1b4": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=4", "-DFSB_MEM_WINDOW=512"],
     "l2_p4b2": ["-DFSB_PAIRS=4", "-DFSB_MIN_BLOCKS=2", "-DFSB_MEM_WINDOW=1024"],
 }
 
 
-def build():
+def build(names=None):
     from paper_2507_20173_b200 import _build
 
     os.makedirs(OUT, exist_ok=True)
     for name, flags in VARIANTS.items():
+        if names and name not in names:
+            continue
         lib = os.path.join(OUT, f"libfsb_{name}.so")
         cmd = [_build.nvcc(), *_build.NVCC_FLAGS, *flags, "-Xptxas", "-v", "-I", _build.INCLUDE, "-I",
                _build.CSRC, *[os.path.join(_build.CSRC, s) for s in _build.SOURCES], "-o", lib, "-ldl"]
@@ -85,14 +91,14 @@ def run(only: str, reps: int, names=None):
 
 
 if __name__ == "__main__":
+    names = None
+    if "--names" in sys.argv:
+        names = sys.argv[sys.argv.index("--names") + 1].split(",")
     if sys.argv[1] == "build":
-        build()
+        build(names)
     else:
         only = "C0,C1"
         reps = 5
         if "--only" in sys.argv:
             only = sys.argv[sys.argv.index("--only") + 1]
-        names = None
-        if "--names" in sys.argv:
-            names = sys.argv[sys.argv.index("--names") + 1].split(",")
         run(only, reps, names)
