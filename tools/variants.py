@@ -7,7 +7,9 @@
 Variants live in build/variants/ (git-ignored, travels to the GPU box).
 Experiments that lost and were removed from the sources after measurement
 (per-thread cp.async prefetch ring, L2 bulk prefetch, bulk ring with STG
-stores, IMAD.HI shifts, one fish per thread) are in profiles/r0*_variants.jsonl.
+stores, IMAD.HI shifts, one fish per thread) are in profiles/r0*_variants.jsonl;
+L2 evict_last carry-over and the cluster grid's predrawn RNG in
+profiles/r04_ab_session.jsonl.
 """
 from __future__ import annotations
 
