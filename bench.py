@@ -173,6 +173,12 @@ def cpu_baseline_sample(n: int, steps: int):
     }
 
 
+def workload(n_per_gpu: int, world: int) -> str:
+    """The config.workload string both arms print (the driver pairs them)."""
+    return (f"FSB {n_per_gpu} fish per GPU fp64 SoA, pond 200, w0 1.0, step_base 0.1, "
+            f"seed 7 (BASELINE configs[1]); {n_per_gpu * world} fish total")
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference's own CPU implementation (oracle/_ref =
     the reference headers compiled with its flags) on all host threads, with its
@@ -205,8 +211,8 @@ def run_reference(args, world, rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (reference init_school, seed 7)",
-        "config": {"workload": f"FSB {n} fish fp64, pond 200, w0 1.0, step_base 0.1, seed 7 (BASELINE configs[1])",
-                   "fish": n, "parallelism": f"cpu {threads} threads"},
+        "config": {"workload": workload(n, world), "fish": n, "parallelism": f"cpu {threads} threads",
+                   "sample": f"{n} fish (the per-GPU school) on the host"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -352,8 +358,7 @@ def run_ours(args, world, rank, local):
             "dtype": "f64",
             "data": "synthetic (reference init_school on device, seed 7)",
             "config": {
-                "workload": f"FSB {n_local} fish per GPU fp64 SoA, pond 200, w0 1.0, step_base 0.1, "
-                            f"seed 7 (BASELINE configs[1]); {n_total} fish total",
+                "workload": workload(n_local, world),
                 "fish_per_gpu": n_local,
                 "fish_total": n_total,
                 "parallelism": f"fish-sharded x{world}" + (" + NCCL allgather(4 fp64)/step" if world > 1 else ""),

@@ -434,12 +434,15 @@ def test_time_step_kernels_keeps_state_valid(orc):
         assert eng.download().tobytes() == fish.tobytes()
 
 
-def test_force_nccl_world1(orc):
-    """The NCCL exchange path (allgather in the graph) on one rank."""
+@pytest.mark.parametrize("kernel", ["static", "dynamic"])
+def test_force_nccl_world1(orc, kernel):
+    """The NCCL exchange path (allgather in the graph) on one rank, with both
+    step kernels (the claimed-tile one is the multi-GPU bench's: 1e7 per GPU)."""
     cfg = fsb.baseline_config(100_000, 8)
     uid = fsb.nccl_unique_id()
     want_fish, want_trace = orc.simulate(ocfg(cfg))
-    with make(cfg, "stream", nccl_unique_id=uid, force_nccl=True) as eng:
+    with make(cfg, "stream", nccl_unique_id=uid, force_nccl=True,
+              **({"static_tiles": True} if kernel == "static" else {"dynamic_tiles": True})) as eng:
         trace, _, _ = eng.simulate(barycentre=False)
         assert trace.tobytes() == want_trace.tobytes()
         assert eng.download().tobytes() == want_fish.tobytes()
@@ -463,14 +466,15 @@ def test_nccl_before_torch_import():
     assert r.returncode == 0, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("n,t", [(100_001, 9), (4096, 30), (1, 5), (0, 3)])
-def test_peer_exchange_world1(orc, n, t):
+@pytest.mark.parametrize("n,t,kw", [(100_001, 9, {}), (100_001, 9, {"dynamic_tiles": True}), (4096, 30, {}),
+                                    (1, 5, {}), (0, 3, {})])
+def test_peer_exchange_world1(orc, n, t, kw):
     """FSB_FLAG_PEER_EXCHANGE on one rank: the step kernel pushes its partial
     into the (self-mapped) peer window and the next kernel acquires the epoch
     flag -- the same code path the NVLink exchange takes across GPUs."""
     cfg = fsb.baseline_config(n, t)
     want_fish, want_trace = orc.simulate(ocfg(cfg))
-    with make(cfg, "auto", peer=True) as eng:
+    with make(cfg, "auto", peer=True, **kw) as eng:
         trace, bary, _ = eng.simulate(barycentre=True)
         assert trace.tobytes() == want_trace.tobytes()
         assert eng.download().tobytes() == want_fish.tobytes()
