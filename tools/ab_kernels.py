@@ -16,6 +16,7 @@ KERNELS = {
     "static": dict(static_tiles=True),  # 4 CTAs per SM, one static chunk each
     "auto": dict(),
     "cgrid": dict(strategy="grid"),               # cooperative persistent, cluster-reduced exchange
+    "persistent": dict(strategy="persistent"),    # one thread-block cluster, state on chip
     "flatgrid": dict(strategy="grid", flat_grid=True),
     "bulk": dict(bulk=True),          # cp.async.bulk shared-memory ring
 }
