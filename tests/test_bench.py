@@ -56,3 +56,14 @@ def test_bench_torchrun_nccl_path():
              "--master-port", str(free_port()), "bench.py", "--gpus", "1", "--steps", "4", "--warmup", "3",
              "--fish", "4000000", "--force-nccl", "--no-cpu-baseline"])
     assert d["value"] > 0 and d["roofline"]["kernel"] == "step_kernel_dyn"
+
+
+def test_reference_arm_under_torchrun():
+    """N>1 launch of the reference arm: rank 0 alone prints the line, the other
+    ranks exit 0 without work."""
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libfsbref.so")):
+        pytest.skip("oracle/_ref not built")
+    d = run(["-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+             "--master-port", str(free_port()), "bench.py", "--impl", "reference", "--gpus", "2", "--steps", "3",
+             "--warmup", "3", "--fish", "20000"])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
