@@ -570,14 +570,19 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(cons
 
 // ---------------------------------------------------------------------------
 // step_kernel_dyn: the same fused pass, one 1024-thread CTA per SM, with the
-// CTA's chunk cut into at most kDynTiles tiles that its warps CLAIM from a
+// CTA's share cut into at most kDynTiles tiles that its warps CLAIM from a
 // shared-memory counter.  With several CTAs per SM the oldest ones win the
 // warp scheduler and the last CTA finishes alone at low occupancy (a 90-120 us
 // spread across CTAs of one step at 1e7 fish, profiles/r03_grid_ctas.jsonl);
-// claiming keeps every warp busy until the chunk is done.  Each tile's partial
-// is accumulated in a fixed order by whichever warp takes it and stored in its
-// own slot, and the slots are folded in tile order, so the sums stay
-// deterministic.  Odd steps claim tiles from the end (L2 reuse, as in step_chunk).
+// claiming keeps every warp busy until the share is done.  The share is a set
+// of stripes of >= kDynMinGroups 32-pair groups dealt round-robin to the CTAs,
+// so all SMs stream one moving front of the arrays (0-3% faster at 1e7 fish
+// than one contiguous chunk per CTA, FSB_DYN_STRIPED=0; the memory-only probe
+// shows 3%, profiles/r04_memory_bound_probe.jsonl).  Each tile's partial is
+// accumulated in a fixed order by whichever warp takes it and stored in its own
+// slot, and the slots are folded in tile order, so the sums stay
+// deterministic.  Odd steps claim tiles from the end, so the front runs
+// backwards over the lines the previous step wrote last (L2 reuse).
 template <bool kExplicitCur, bool kSane>
 __global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs a) {
     __shared__ Partial tile_part[kDynTiles];
@@ -598,6 +603,20 @@ __global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs
     // balanced contiguous chunk of 32-pair groups (32-bit group indices: up
     // to 2^37 fish per shard); tiles of gpt groups
     const uint64_t ngroups_all = (npairs + 31) / 32;
+#if FSB_DYN_STRIPED
+    // stripes of gpt groups dealt round-robin to the CTAs (tile k of this CTA
+    // is stripe k * gridDim + blockIdx.x): every SM works on one moving front
+    unsigned gpt = (unsigned)((ngroups_all + (uint64_t)gridDim.x * kDynTiles - 1) / ((uint64_t)gridDim.x * kDynTiles));
+    if (gpt < kDynMinGroups) gpt = kDynMinGroups;
+    const unsigned nstripes = (unsigned)((ngroups_all + gpt - 1) / gpt);
+    if (threadIdx.x == 0) {
+        next_tile = 0;
+        s_glo = 0;
+        s_ghi = (unsigned)ngroups_all;
+        s_gpt = gpt;
+        s_ntiles = nstripes > blockIdx.x ? (nstripes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    }
+#else
     const unsigned g_lo = (unsigned)(ngroups_all * blockIdx.x / gridDim.x);
     const unsigned g_hi = (unsigned)(ngroups_all * (blockIdx.x + 1) / gridDim.x);
     const unsigned ngroups = g_hi - g_lo;
@@ -610,6 +629,7 @@ __global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs
         s_gpt = gpt;
         s_ntiles = gpt ? (ngroups + gpt - 1) / gpt : 0u;
     }
+#endif
     __syncthreads();
 
     double2* X2 = reinterpret_cast<double2*>(a.s.x);
@@ -639,7 +659,11 @@ __global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs
             FSB_CHECK(nt <= (unsigned)kDynTiles && tile < nt);
             const unsigned gpt_ = *(volatile unsigned*)&s_gpt;
             const unsigned gh = *(volatile unsigned*)&s_ghi;
+#if FSB_DYN_STRIPED
+            grp = (tile * gridDim.x + blockIdx.x) * gpt_;
+#else
             grp = *(volatile unsigned*)&s_glo + tile * gpt_;
+#endif
             gend = (grp + gpt_ < gh) ? grp + gpt_ : gh;
         }
         const uint64_t q = (uint64_t)grp * 32 + lane;

@@ -87,6 +87,9 @@ constexpr int kDynTiles = 1024;   // tile-partial slots per CTA (32 KB of shared
 #define FSB_DYN_MIN_GROUPS 4
 #endif
 constexpr unsigned kDynMinGroups = FSB_DYN_MIN_GROUPS;  // minimum 32-pair groups per claimed tile
+#ifndef FSB_DYN_STRIPED
+#define FSB_DYN_STRIPED 1  // claimed tiles are stripes dealt round-robin to the CTAs (one front); 0: one contiguous chunk per CTA
+#endif
 constexpr int kTileFish = 2 * kTilePairs;
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,

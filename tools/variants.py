@@ -51,6 +51,8 @@ VARIANTS = {
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
+    # claimed-tile kernel: one contiguous chunk per CTA instead of round-robin stripes
+    "chunked": ["-DFSB_DYN_STRIPED=0"],
     # claimed-tile kernel: minimum 32-pair groups per tile
     "dg1": ["-DFSB_DYN_MIN_GROUPS=1"],
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
