@@ -256,6 +256,36 @@ def issue_roofline(n: int, kernel: str, kernel_s: float, clocks: dict):
             "note": "issue-active fraction the step kernel sustains; with HBM frac_moved ~0.8 both limits bind"}
 
 
+def same_bytes_memory_bound(state_bytes: int, device: int):
+    """Memory-only kernels over the step's own traffic (the state read and
+    written once): torch's in-place fp64 add (the step's in-place pattern) and
+    an out-of-place copy, best of 5 with CUDA events.  At 320 MB they run below
+    the 4 GB copy of MEASURED_PEAKS.json (launch ramp and tail), so they are
+    the practical bound the step kernel is compared with."""
+    import torch
+
+    n = state_bytes // 8
+    a = torch.ones(n, dtype=torch.float64, device=f"cuda:{device}")
+    b = torch.empty_like(a)
+    out = {}
+    for name, fn in (("inplace_add", lambda: a.add_(1.0)), ("copy", lambda: b.copy_(a))):
+        for _ in range(3):
+            fn()
+        best = None
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            t = e0.elapsed_time(e1) * 1e-3
+            best = t if best is None else min(best, t)
+        out[name] = {"us": best * 1e6, "gbs": 2 * state_bytes / best / 1e9}
+    del a, b
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, world, rank, local):
     import ctypes
 
@@ -306,6 +336,7 @@ def run_ours(args, world, rank, local):
     _, cta_threads = eng.grid()
     kernel = "step_kernel_dyn" if cta_threads == 1024 else ("step_kernel_bulk" if args.bulk else "step_kernel")
     traffic, traffic_src = load_profile_traffic(n_local, kernel)
+    same_bytes = same_bytes_memory_bound(n_local * MOVED_BYTES_PER_UPDATE // 2, local)
 
     # e2e through the C-ABI with host buffers (pinned), all copies timed
     e2e = None
@@ -382,6 +413,9 @@ def run_ours(args, world, rank, local):
                         "per fish-update against the 80 B algorithmic figure, so frac on 80 B can reach "
                         "1.25 at the HBM limit; the kernel is co-limited by instruction issue (DESIGN.md)",
                 "kernel_ms": kernel_s * 1e3,
+                "same_bytes_memory_only": same_bytes,
+                "frac_vs_same_bytes_inplace": (same_bytes["inplace_add"]["us"] * 1e-6 / kernel_s
+                                               if same_bytes else None),
                 "peak_source": peak_src,
                 "traffic_source": traffic_src,
             },
