@@ -334,7 +334,7 @@ def run_ours(args, world, rank, local):
     peak_gbs, peak_src = peaks()
     achieved = BYTES_PER_UPDATE * n_local / kernel_s / 1e9
     _, cta_threads = eng.grid()
-    kernel = "step_kernel_dyn" if cta_threads == 1024 else ("step_kernel_bulk" if args.bulk else "step_kernel")
+    kernel = "step_kernel_bulk" if args.bulk else ("step_kernel" if cta_threads == 256 else "step_kernel_dyn")
     traffic, traffic_src = load_profile_traffic(n_local, kernel)
     same_bytes = same_bytes_memory_bound(n_local * MOVED_BYTES_PER_UPDATE // 2, local)
 

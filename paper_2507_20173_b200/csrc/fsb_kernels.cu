@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(cons
 // deterministic.  Odd steps claim tiles from the end, so the front runs
 // backwards over the lines the previous step wrote last (L2 reuse).
 template <bool kExplicitCur, bool kSane>
-__global__ void __launch_bounds__(kDynThreads, 1) step_kernel_dyn(const StepArgs a) {
+__global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_dyn(const StepArgs a) {
     __shared__ Partial tile_part[kDynTiles];
     // tile bookkeeping lives in shared memory, not in registers: the hot loop
     // is at the 64-register limit of 1024-thread CTAs

@@ -81,7 +81,13 @@ constexpr int kPairsPerThread = FSB_PAIRS;  // double2 loads per array per threa
 constexpr int kTilePairs = kStepThreads * kPairsPerThread;
 
 // step_kernel_dyn: one CTA per SM, warps claim tiles of its chunk.
-constexpr int kDynThreads = 1024;
+#ifndef FSB_DYN_THREADS
+#define FSB_DYN_THREADS 1024
+#endif
+#ifndef FSB_DYN_MIN_BLOCKS
+#define FSB_DYN_MIN_BLOCKS 1
+#endif
+constexpr int kDynThreads = FSB_DYN_THREADS;
 constexpr int kDynTiles = 1024;   // tile-partial slots per CTA (32 KB of shared memory)
 #ifndef FSB_DYN_MIN_GROUPS
 #define FSB_DYN_MIN_GROUPS 4

@@ -51,6 +51,10 @@ VARIANTS = {
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
+    # claimed-tile kernel: CTA size x CTAs per SM (default 1024 x 1, 64 registers)
+    "d576x2": ["-DFSB_DYN_THREADS=576", "-DFSB_DYN_MIN_BLOCKS=2"],
+    "d384x3": ["-DFSB_DYN_THREADS=384", "-DFSB_DYN_MIN_BLOCKS=3"],
+    "d640x2": ["-DFSB_DYN_THREADS=640", "-DFSB_DYN_MIN_BLOCKS=2"],
     # claimed-tile kernel: one contiguous chunk per CTA instead of round-robin stripes
     "chunked": ["-DFSB_DYN_STRIPED=0"],
     # claimed-tile kernel: minimum 32-pair groups per tile
