@@ -1126,6 +1126,13 @@ __global__ void aos_to_soa_kernel(const FishAoS* in, SoA s, double half, uint64_
 // (it needs their next partials first), so no further synchronisation is needed.
 
 constexpr int kMaxCluster = 16;
+#ifndef FSB_CLUSTER_F
+#define FSB_CLUSTER_F 1
+#endif
+constexpr int kClusterF = FSB_CLUSTER_F;  // fish per thread of the persistent cluster kernel
+#ifndef FSB_CLUSTER_EXP
+#define FSB_CLUSTER_EXP 0  // experiment builds only (tools/variants.py cexp1 / cexp2): results are not the reference's
+#endif
 
 __device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem, unsigned rank) {
     uint32_t r;
@@ -1206,7 +1213,8 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     for (uint64_t k = 0; k < a.num_steps; ++k) {
         const uint64_t step = a.first_step + k;
         const unsigned b = (unsigned)(k & 1);
-        if (threadIdx.x == 0) mbar_expect_tx(&xbar[b], ncta * kBytes);  // may race the pushes: fine
+        if (threadIdx.x == 0 && (FSB_CLUSTER_EXP == 0 || kBary))
+            mbar_expect_tx(&xbar[b], ncta * kBytes);  // may race the pushes: fine
         const bool eat = M > 0.0;
         const SharedDivisor D = make_divisor(eat ? M : 1.0);
         Partial acc = identity();
@@ -1225,6 +1233,26 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
                 }
             }
         }
+#if FSB_CLUSTER_EXP == 1  // experiment: warp-local max only (no block reduction, no exchange)
+        if (!kBary) {
+#pragma unroll
+            for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
+            M = warp_max_redux(acc.best);
+            if (crank == 0 && threadIdx.x == 0) a.trace[k] = M;
+            continue;
+        }
+#elif FSB_CLUSTER_EXP == 2  // experiment: block reduction, no cluster exchange
+        if (!kBary) {
+            const double bm = block_reduce_max(acc.best, scratch_max);
+#pragma unroll
+            for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
+            if (threadIdx.x == 0) slots[b][0].best = bm;
+            __syncthreads();
+            M = slots[b][0].best;
+            if (crank == 0 && threadIdx.x == 0) a.trace[k] = M;
+            continue;
+        }
+#endif
         Partial blk = identity();
         if (kBary) blk = block_reduce(acc, scratch);
         else blk.best = block_reduce_max(acc.best, scratch_max);
@@ -1692,6 +1720,8 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
     if (!cached) {
         cudaFuncSetAttribute(cluster_kernel<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cudaFuncSetAttribute(cluster_kernel<1, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(cluster_kernel<kClusterF, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(cluster_kernel<kClusterF, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cached = 8;
         for (int c : {16, 8}) {
             cudaLaunchConfig_t cfg = {};
@@ -1732,7 +1762,7 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     if (ncta < 1) ncta = 1;
     const uint64_t per_cta = (a.n + ncta - 1) / ncta;
     if (per_cta > 1024) return cudaErrorNotSupported;
-    const uint64_t threads = ((per_cta + 31) / 32) * 32;
+    const uint64_t threads = ((per_cta + kClusterF * 32 - 1) / (kClusterF * 32)) * 32;  // kClusterF fish per thread
 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)ncta);
@@ -1745,8 +1775,8 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<1, true>, a);
-    return cudaLaunchKernelEx(&cfg, cluster_kernel<1, false>, a);
+    if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true>, a);
+    return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false>, a);
 }
 
 }  // namespace fsb_dev

@@ -51,6 +51,13 @@ VARIANTS = {
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
+    # experiment: persistent cluster kernel without the exchange (1: warp max only, 2: block max only)
+    "cexp1": ["-DFSB_CLUSTER_EXP=1"],
+    "cexp2": ["-DFSB_CLUSTER_EXP=2"],
+    # persistent cluster kernel: fish per thread
+    "cf2": ["-DFSB_CLUSTER_F=2"],
+    "cf2m512": ["-DFSB_CLUSTER_F=2", "-DFSB_CLUSTER_MIN_FISH=512"],
+    "cf4": ["-DFSB_CLUSTER_F=4"],
     # claimed-tile kernel: CTA size x CTAs per SM (default 1024 x 1, 64 registers)
     "d576x2": ["-DFSB_DYN_THREADS=576", "-DFSB_DYN_MIN_BLOCKS=2"],
     "d384x3": ["-DFSB_DYN_THREADS=384", "-DFSB_DYN_MIN_BLOCKS=3"],
