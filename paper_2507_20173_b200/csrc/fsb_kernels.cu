@@ -109,25 +109,36 @@ __device__ __forceinline__ double warp_max_redux(double v) {
     return __longlong_as_double(static_cast<long long>(bits));
 }
 
-__device__ __forceinline__ double warp_reduce_max(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const double u = __shfl_xor_sync(0xffffffffu, v, o);
-        v = (u > v) ? u : v;
-    }
-    return v;
+// The same max carried as keys through a multi-level reduction (the
+// persistent cluster kernel): encode once per thread, decode once after the
+// last level.
+constexpr unsigned long long kKeyNegInf = ~0xfff0000000000000ull;  // max_key(-inf)
+__device__ __forceinline__ unsigned long long max_key(double v) {
+    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+    if (v != v) b = 0xfff0000000000000ull;  // NaN -> -inf
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
-
-__device__ __forceinline__ double block_reduce_max(double v, double* scratch) {
+__device__ __forceinline__ double key_value(unsigned long long m) {
+    const unsigned long long bits = (m >> 63) ? (m & 0x7fffffffffffffffull) : ~m;
+    return __longlong_as_double(static_cast<long long>(bits));
+}
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long key) {
+    const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(key >> 32));
+    const unsigned lo = __reduce_max_sync(
+        0xffffffffu, static_cast<unsigned>(key >> 32) == hi ? static_cast<unsigned>(key) : 0u);
+    return (static_cast<unsigned long long>(hi) << 32) | lo;
+}
+// valid in warp 0 (all lanes)
+__device__ __forceinline__ unsigned long long block_max_key(unsigned long long key, unsigned long long* scratch) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    v = warp_max_redux(v);
-    if (lane == 0) scratch[warp] = v;
+    key = warp_max_key(key);
+    if (lane == 0) scratch[warp] = key;
     __syncthreads();
-    double r = -INFINITY;
+    unsigned long long r = kKeyNegInf;
     if (warp == 0) {
         if (lane < (int)(blockDim.x >> 5)) r = scratch[lane];
-        r = warp_max_redux(r);
+        r = warp_max_key(r);
     }
     return r;
 }
@@ -1172,7 +1183,7 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     __shared__ __align__(16) Partial slots[2][kMaxCluster];
     __shared__ __align__(8) uint64_t xbar[2];
     __shared__ Partial scratch[32];
-    __shared__ double scratch_max[32];
+    __shared__ unsigned long long scratch_key[32];
     constexpr unsigned kBytes = kBary ? 32 : 8;  // bytes each CTA pushes per destination
     if (threadIdx.x == 0) {
         mbar_init(&xbar[0], 1);
@@ -1243,7 +1254,7 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         }
 #elif FSB_CLUSTER_EXP == 2  // experiment: block reduction, no cluster exchange
         if (!kBary) {
-            const double bm = block_reduce_max(acc.best, scratch_max);
+            const double bm = key_value(block_max_key(max_key(acc.best), scratch_key));
 #pragma unroll
             for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
             if (threadIdx.x == 0) slots[b][0].best = bm;
@@ -1255,7 +1266,8 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
 #endif
         Partial blk = identity();
         if (kBary) blk = block_reduce(acc, scratch);
-        else blk.best = block_reduce_max(acc.best, scratch_max);
+        else  // the CTA max travels as its key (bits in .best), decoded after the fold
+            blk.best = __longlong_as_double(static_cast<long long>(block_max_key(max_key(acc.best), scratch_key)));
         if (threadIdx.x < 32 && threadIdx.x < ncta) {  // lane r pushes this CTA's partial to CTA r
             const uint32_t dst = cluster_map(smem_u32(&slots[b][crank]), threadIdx.x);
             const uint32_t bar = cluster_map(smem_u32(&xbar[b]), threadIdx.x);
@@ -1276,7 +1288,9 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
             tot = warp_reduce(lane < ncta ? slots[k & 1][lane] : identity());
         } else {  // every warp folds the <= 16 CTA maxima itself: one LDS + two REDUX
             const unsigned lane = threadIdx.x & 31;
-            tot.best = warp_max_redux(lane < ncta ? slots[k & 1][lane].best : -INFINITY);
+            tot.best = key_value(warp_max_key(
+                lane < ncta ? static_cast<unsigned long long>(__double_as_longlong(slots[k & 1][lane].best))
+                            : kKeyNegInf));
         }
         M = tot.best;
         if (crank == 0 && threadIdx.x == 0) {
