@@ -97,21 +97,8 @@ __device__ __forceinline__ Partial block_reduce(Partial v, Partial* scratch) {
 // high words, then max of the low words among the lanes that hold that high
 // word.  NaN maps to the key of -inf, so -- as in the reference's strict '>'
 // fold (executor.hpp:90) -- it never wins.
-__device__ __forceinline__ double warp_max_redux(double v) {
-    unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
-    if (v != v) b = 0xfff0000000000000ull;  // NaN -> -inf
-    const unsigned long long key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-    const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(key >> 32));
-    const unsigned lo = __reduce_max_sync(
-        0xffffffffu, static_cast<unsigned>(key >> 32) == hi ? static_cast<unsigned>(key) : 0u);
-    const unsigned long long m = (static_cast<unsigned long long>(hi) << 32) | lo;
-    const unsigned long long bits = (m >> 63) ? (m & 0x7fffffffffffffffull) : ~m;
-    return __longlong_as_double(static_cast<long long>(bits));
-}
-
-// The same max carried as keys through a multi-level reduction (the
-// persistent cluster kernel): encode once per thread, decode once after the
-// last level.
+// The max is carried as a key through a multi-level reduction (the persistent
+// cluster kernel): encode once per thread, decode once after the last level.
 constexpr unsigned long long kKeyNegInf = ~0xfff0000000000000ull;  // max_key(-inf)
 __device__ __forceinline__ unsigned long long max_key(double v) {
     unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
