@@ -365,6 +365,9 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
     ee = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ee != cudaSuccess) return cuda_fail(ee, "cudaGraphInstantiate");
+    // upload the executable graph now, not as part of its first (timed) launch
+    ee = cudaGraphUpload(g.exec, e->stream);
+    if (ee != cudaSuccess) return cuda_fail(ee, "cudaGraphUpload");
     g.launches = launches;
     *out = g;
     return FSB_OK;
