@@ -9,9 +9,11 @@
 //   aosoa_pp   ping-pong AoSoA
 //   copy       plain grid-stride copy of the same bytes (calibration)
 //   soa_gs     soa, grid-stride over groups (one moving front; 148 x 1024 and, soa_gs4, 592 x 256)
-//   soa_many   soa, one short 256-thread CTA per 256 pairs (torch-style grid)
-// Prints device time per pass and GB/s of bytes moved (64 B per fish-pair read + written... per pair 128 B).
+//   soa_many   soa, one short 256-thread CTA per 256 pairs (torch-style grid, 2048 threads per SM)
+//   soa_many_occ4 / _occ2 / soa_many512_occ2   the same capped at 4 / 2 CTAs per SM by dynamic shared memory
+// Prints device time per pass and GB/s moved (128 B per fish pair: 64 B read + 64 B written).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/layout_probe tools/layout_probe.cu
+//   ./build/layout_probe [fish]            (results: profiles/r04_memory_bound_probe.jsonl)
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
