@@ -1659,6 +1659,10 @@ cudaLaunchConfig_t cgrid_config(int clusters, cudaStream_t st, cudaLaunchAttribu
 
 int cgrid_clusters(int device) {
     (void)device;
+    if (kCGridCluster > 8) {  // non-portable cluster sizes (experiment builds)
+        cudaFuncSetAttribute(cgrid_kernel<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaFuncSetAttribute(cgrid_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
     cudaLaunchAttribute at[2];
     cudaLaunchConfig_t cfg = cgrid_config(1, nullptr, at);
     int n0 = 0, n1 = 0;

@@ -48,6 +48,7 @@ VARIANTS = {
     # cluster-reduced grid kernel: CTAs per cluster
     "cg2": ["-DFSB_CGRID_CLUSTER=2"],
     "cg4": ["-DFSB_CGRID_CLUSTER=4"],
+    "cg16": ["-DFSB_CGRID_CLUSTER=16"],
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
