@@ -6,10 +6,16 @@
 //                   objective (sim.hpp:90-98), and this step's partial
 //                   max(prev-cur) (sim.hpp:112-114) plus the f-weighted
 //                   barycentre sums, reduced warp -> CTA -> grid (last CTA).
-//                   double2 loads/stores, two fish per thread (the default).
+//                   double2 loads/stores, two fish per thread; one static
+//                   chunk per 256-thread CTA (shards below 3e6 fish).
+//   step_kernel_dyn the same pass, one 1024-thread CTA per SM whose warps
+//                   claim tiles (round-robin stripes) and draw their RNG ahead
+//                   of the loaded state (the default from 3e6 fish: C1-C3).
 //   step_kernel_bulk  the same pass streamed through a shared-memory ring by
 //                   cp.async.bulk + mbarriers (FSB_FLAG_FORCE_BULK, A/B).
-//   grid_kernel     all T steps in one cooperative launch (FSB_STRATEGY_GRID).
+//   grid_kernel     all T steps in one cooperative launch (FSB_FLAG_FLAT_GRID).
+//   cgrid_kernel    the same with 8-CTA clusters reducing over DSMEM before the
+//                   grid-wide exchange (FSB_STRATEGY_GRID; AUTO 16,385-2.5e6 fish).
 //   eat_kernel      the trailing / standalone weight update (sim.hpp:115-121).
 //   reduce_kernel   max + sums of the current state without moving it (eat()
 //                   after an upload).
