@@ -163,7 +163,9 @@ struct fsb_engine {
     double* d_cl_slots = nullptr;            // [kSlotRing][cgrid_nc][kSlotWords]
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
 
-    void* staging = nullptr;  // device AoS staging
+    void* staging = nullptr;  // device AoS staging (two halves of kStagingFish / 2 fish: double-buffered transfers)
+    cudaStream_t xfer = nullptr;        // copy stream of upload / download (overlaps the transposes)
+    cudaEvent_t ev_half[2][2] = {};     // per staging half: [0] copy done, [1] transpose done
     void* pinned = nullptr;   // host pinned staging (checksum)
     double* d_cl_trace = nullptr;  // persistent-kernel trace buffers
     double* d_cl_bary = nullptr;
@@ -221,6 +223,11 @@ int guard(fsb_engine* e) {
 
 int ensure_staging(fsb_engine* e) {
     if (!e->staging) CU(cudaMalloc(&e->staging, kStagingFish * sizeof(fsb_fish)));
+    if (!e->xfer) {
+        CU(cudaStreamCreateWithFlags(&e->xfer, cudaStreamNonBlocking));
+        for (auto& h : e->ev_half)
+            for (auto& v : h) CU(cudaEventCreateWithFlags(&v, cudaEventDisableTiming));
+    }
     return FSB_OK;
 }
 
@@ -644,6 +651,13 @@ int fsb_engine_destroy(fsb_engine* e) {
     if (e->pinned) cudaFreeHost(e->pinned);
     if (e->ev0) cudaEventDestroy(e->ev0);
     if (e->ev1) cudaEventDestroy(e->ev1);
+    for (auto& h : e->ev_half)
+        for (auto& v : h)
+            if (v) cudaEventDestroy(v);
+    if (e->xfer) {
+        cudaStreamSynchronize(e->xfer);
+        cudaStreamDestroy(e->xfer);
+    }
     if (e->stream) cudaStreamDestroy(e->stream);
     delete e;
     return FSB_OK;
@@ -807,10 +821,22 @@ int fsb_engine_upload(fsb_engine* e, const fsb_fish* fish, uint64_t count) {
     fsb_dev::SoA s = e->s;
     s.c = e->c_buf;
     CU(cudaMemsetAsync(e->d_mismatch, 0, sizeof(int), e->stream));
-    for (uint64_t lo = 0; lo < count; lo += kStagingFish) {
-        const uint64_t cnt = (count - lo < kStagingFish) ? count - lo : kStagingFish;
-        CU(cudaMemcpyAsync(e->staging, fish + lo, cnt * sizeof(fsb_fish), cudaMemcpyHostToDevice, e->stream));
-        CU(fsb_dev::launch_aos_to_soa(e->staging, s, e->cfg.pond_size / 2.0, lo, cnt, e->d_mismatch, e->stream));
+    // chunk i: H2D into staging half i&1 on the copy stream, transpose on the
+    // engine stream; the copy of chunk i+1 runs while chunk i is transposed
+    constexpr uint64_t kHalf = kStagingFish / 2;
+    CU(cudaEventRecord(e->ev_half[0][1], e->stream));  // both halves free, ordered after prior work
+    CU(cudaEventRecord(e->ev_half[1][1], e->stream));
+    uint64_t i = 0;
+    for (uint64_t lo = 0; lo < count; lo += kHalf, ++i) {
+        const int h = (int)(i & 1);
+        const uint64_t cnt = (count - lo < kHalf) ? count - lo : kHalf;
+        fsb_fish* half = static_cast<fsb_fish*>(e->staging) + h * kHalf;
+        CU(cudaStreamWaitEvent(e->xfer, e->ev_half[h][1], 0));
+        CU(cudaMemcpyAsync(half, fish + lo, cnt * sizeof(fsb_fish), cudaMemcpyHostToDevice, e->xfer));
+        CU(cudaEventRecord(e->ev_half[h][0], e->xfer));
+        CU(cudaStreamWaitEvent(e->stream, e->ev_half[h][0], 0));
+        CU(fsb_dev::launch_aos_to_soa(half, s, e->cfg.pond_size / 2.0, lo, cnt, e->d_mismatch, e->stream));
+        CU(cudaEventRecord(e->ev_half[h][1], e->stream));
     }
     int mismatch = 0;
     CU(cudaMemcpyAsync(&mismatch, e->d_mismatch, sizeof(int), cudaMemcpyDeviceToHost, e->stream));
@@ -827,11 +853,24 @@ int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count) {
     if (count && !fish) return fail(FSB_ERR_INVALID_ARGUMENT, "null fish");
     TRY(ensure_staging(e));
     const fsb_dev::SoA s = canonical(e);
-    for (uint64_t lo = 0; lo < count; lo += kStagingFish) {
-        const uint64_t cnt = (count - lo < kStagingFish) ? count - lo : kStagingFish;
-        CU(fsb_dev::launch_soa_to_aos(s, e->cfg.pond_size / 2.0, lo, cnt, e->staging, e->stream));
-        CU(cudaMemcpyAsync(fish + lo, e->staging, cnt * sizeof(fsb_fish), cudaMemcpyDeviceToHost, e->stream));
+    // chunk i: transpose into staging half i&1 on the engine stream, D2H on the
+    // copy stream; the transpose of chunk i+1 runs while chunk i is copied
+    constexpr uint64_t kHalf = kStagingFish / 2;
+    CU(cudaEventRecord(e->ev_half[0][0], e->xfer));  // both halves free
+    CU(cudaEventRecord(e->ev_half[1][0], e->xfer));
+    uint64_t i = 0;
+    for (uint64_t lo = 0; lo < count; lo += kHalf, ++i) {
+        const int h = (int)(i & 1);
+        const uint64_t cnt = (count - lo < kHalf) ? count - lo : kHalf;
+        fsb_fish* half = static_cast<fsb_fish*>(e->staging) + h * kHalf;
+        CU(cudaStreamWaitEvent(e->stream, e->ev_half[h][0], 0));
+        CU(fsb_dev::launch_soa_to_aos(s, e->cfg.pond_size / 2.0, lo, cnt, half, e->stream));
+        CU(cudaEventRecord(e->ev_half[h][1], e->stream));
+        CU(cudaStreamWaitEvent(e->xfer, e->ev_half[h][1], 0));
+        CU(cudaMemcpyAsync(fish + lo, half, cnt * sizeof(fsb_fish), cudaMemcpyDeviceToHost, e->xfer));
+        CU(cudaEventRecord(e->ev_half[h][0], e->xfer));
     }
+    CU(cudaStreamSynchronize(e->xfer));
     CU(cudaStreamSynchronize(e->stream));
     return FSB_OK;
 }
