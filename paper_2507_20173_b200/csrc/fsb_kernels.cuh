@@ -100,7 +100,10 @@ constexpr int kTileFish = 2 * kTilePairs;
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,
 // plus one producer warp; a kBulkStages-deep ring of sub-tiles in smem.
-constexpr int kBulkCompute = 256;
+#ifndef FSB_BULK_COMPUTE
+#define FSB_BULK_COMPUTE 256
+#endif
+constexpr int kBulkCompute = FSB_BULK_COMPUTE;  // compute threads per bulk-ring CTA (+ one producer warp)
 constexpr int kBulkThreads = kBulkCompute + 32;
 constexpr int kBulkPairsPerThread = FSB_BULK_PAIRS;
 constexpr int kBulkTilePairs = kBulkCompute * kBulkPairsPerThread;

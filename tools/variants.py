@@ -38,6 +38,8 @@ VARIANTS = {
     "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b4s2m1": ["-DFSB_BULK_PAIRS=4", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=1"],
     "l2_bulk": ["-DFSB_MEM_WINDOW=512"],
+    # bulk ring with more compute warps per SM (compute threads x stages x CTAs per SM): all slower
+    "bk992s3m1": ["-DFSB_BULK_COMPUTE=992", "-DFSB_BULK_STAGES=3", "-DFSB_BULK_MIN_BLOCKS=1"],
     # LDG kernel with bigger CTAs (fewer CTA partials in the per-step grid reduction)
     "t512b2": ["-DFSB_STEP_THREADS=512", "-DFSB_MIN_BLOCKS=2"],
     "t1024b1": ["-DFSB_STEP_THREADS=1024", "-DFSB_MIN_BLOCKS=1"],
