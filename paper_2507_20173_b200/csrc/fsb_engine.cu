@@ -822,7 +822,16 @@ int fsb_engine_upload(fsb_engine* e, const fsb_fish* fish, uint64_t count) {
     s.c = e->c_buf;
     CU(cudaMemsetAsync(e->d_mismatch, 0, sizeof(int), e->stream));
     // chunk i: H2D into staging half i&1 on the copy stream, transpose on the
-    // engine stream; the copy of chunk i+1 runs while chunk i is transposed
+    // engine stream; the copy of chunk i+1 runs while chunk i is transposed.
+    // On any error both streams are drained before returning (no copy may
+    // still read the caller's buffer).
+    struct Drain {
+        fsb_engine* e;
+        ~Drain() {
+            cudaStreamSynchronize(e->xfer);
+            cudaStreamSynchronize(e->stream);
+        }
+    } drain{e};
     constexpr uint64_t kHalf = kStagingFish / 2;
     CU(cudaEventRecord(e->ev_half[0][1], e->stream));  // both halves free, ordered after prior work
     CU(cudaEventRecord(e->ev_half[1][1], e->stream));
@@ -854,7 +863,15 @@ int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count) {
     TRY(ensure_staging(e));
     const fsb_dev::SoA s = canonical(e);
     // chunk i: transpose into staging half i&1 on the engine stream, D2H on the
-    // copy stream; the transpose of chunk i+1 runs while chunk i is copied
+    // copy stream; the transpose of chunk i+1 runs while chunk i is copied.
+    // Both streams are drained on every return path.
+    struct Drain {
+        fsb_engine* e;
+        ~Drain() {
+            cudaStreamSynchronize(e->xfer);
+            cudaStreamSynchronize(e->stream);
+        }
+    } drain{e};
     constexpr uint64_t kHalf = kStagingFish / 2;
     CU(cudaEventRecord(e->ev_half[0][0], e->xfer));  // both halves free
     CU(cudaEventRecord(e->ev_half[1][0], e->xfer));
@@ -872,7 +889,7 @@ int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count) {
     }
     CU(cudaStreamSynchronize(e->xfer));
     CU(cudaStreamSynchronize(e->stream));
-    return FSB_OK;
+    return FSB_OK;  // (drain: already idle)
 }
 
 int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
