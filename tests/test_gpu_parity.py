@@ -402,6 +402,22 @@ def test_run_split_equals_whole(orc):
         assert a.download().tobytes() == b.download().tobytes()
 
 
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("first", [2**32 + 3, 2**63 + 7, 2**64 - 4])
+def test_large_step_index(orc, strategy, first):
+    """The step index is a full u64 RNG word (rng.hpp:34-36): runs starting
+    anywhere up to just below kInitStep = 2^64-1 match the oracle."""
+    n = 4096 if strategy == "persistent" else 50_001
+    cfg = fsb.baseline_config(n, 3)
+    fish = orc.init(ocfg(cfg))
+    want_trace = orc.run(ocfg(cfg), fish, first, 3)
+    with make(cfg, strategy) as eng:
+        eng.init()
+        trace, _, _ = eng.run(first, 3)
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == fish.tobytes()
+
+
 def test_empty_school():
     cfg = fsb.SimConfig(num_fish=0, num_steps=4)
     with make(cfg) as eng:
