@@ -418,6 +418,19 @@ def test_large_step_index(orc, strategy, first):
         assert eng.download().tobytes() == fish.tobytes()
 
 
+@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("seed", [0, 1, 2**63, 2**64 - 1])
+def test_extreme_seeds(orc, strategy, seed):
+    """Seed words at the ends of the u64 range (the first fold_in operand)."""
+    n = 3000 if strategy == "persistent" else 30_001
+    cfg = fsb.SimConfig(num_fish=n, num_steps=6, seed=seed, pond_size=200.0, weight_scale=1.0, step_base=0.1)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, strategy) as eng:
+        trace, _, _ = eng.simulate(barycentre=False)
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == want_fish.tobytes()
+
+
 def test_empty_school():
     cfg = fsb.SimConfig(num_fish=0, num_steps=4)
     with make(cfg) as eng:
