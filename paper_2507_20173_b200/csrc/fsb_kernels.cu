@@ -643,6 +643,81 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
     const SoA2 src{X2, Y2, W2, P2, C2};
     const unsigned lane = threadIdx.x & 31;
+#if FSB_DYN_PIPE
+    // experiment: register double-buffering -- the next group's loads (claiming
+    // its tile early when the current one ends) are issued before the current
+    // group is computed, so every warp keeps one group in flight while it
+    // computes.  Costs 16-20 registers per thread: fewer, fatter threads per SM.
+    auto claim = [&](unsigned& t_, unsigned& g_, unsigned& e_) -> bool {
+        unsigned c = 0;
+        if (lane == 0) c = atomicAdd(&next_tile, 1u);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const unsigned nt = *(volatile unsigned*)&s_ntiles;
+        if (c >= nt) return false;
+        t_ = rev ? nt - 1 - c : c;
+        const unsigned gpt_ = *(volatile unsigned*)&s_gpt;
+        const unsigned gh = *(volatile unsigned*)&s_ghi;
+#if FSB_DYN_STRIPED
+        g_ = (t_ * gridDim.x + blockIdx.x) * gpt_;
+#else
+        g_ = *(volatile unsigned*)&s_glo + t_ * gpt_;
+#endif
+        e_ = (g_ + gpt_ < gh) ? g_ + gpt_ : gh;
+        return true;
+    };
+    unsigned tile = 0, grp = 0, gend = 0;
+    bool have = claim(tile, grp, gend);
+    Partial acc = identity();
+    double2 X[1], Y[1], W[1], Q[1], C[1];
+    {
+        const uint64_t q = (uint64_t)grp * 32 + lane;
+        if (have && q < npairs) {
+            X[0] = X2[q];
+            Y[0] = Y2[q];
+            W[0] = W2[q];
+            Q[0] = P2[q];
+            if (kExplicitCur) C[0] = C2[q];
+        }
+    }
+    while (have) {
+        unsigned ntile = tile, ngrp = grp + 1, ngend = gend;
+        bool nhave = true;
+        if (ngrp == gend) nhave = claim(ntile, ngrp, ngend);
+        double2 NX, NY, NW, NQ, NC;
+        const uint64_t nq = (uint64_t)ngrp * 32 + lane;
+        if (nhave && nq < npairs) {
+            NX = X2[nq];
+            NY = Y2[nq];
+            NW = W2[nq];
+            NQ = P2[nq];
+            if (kExplicitCur) NC = C2[nq];
+        }
+        const uint64_t q = (uint64_t)grp * 32 + lane;
+        const bool valid[1] = {q < npairs};
+        const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
+        fused_pairs<kExplicitCur, 1, kSane, true>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
+        if (valid[0]) {
+            X2[q] = X[0];
+            Y2[q] = Y[0];
+            W2[q] = W[0];
+            P2[q] = Q[0];
+        }
+        if (!nhave || ntile != tile) {
+            const Partial tp = warp_reduce(acc);
+            if (lane == 0) tile_part[tile] = tp;
+            acc = identity();
+        }
+        X[0] = NX;
+        Y[0] = NY;
+        W[0] = NW;
+        Q[0] = NQ;
+        if (kExplicitCur) C[0] = NC;
+        tile = ntile;
+        grp = ngrp;
+        gend = ngend;
+        have = nhave;
+    }
+#else
     // one loop over groups; a warp claims its next tile when the current one
     // is exhausted (warp-uniform branch), flushing the finished tile's partial
     unsigned grp = 0, gend = 0, tile = ~0u;
@@ -690,6 +765,7 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
         }
         ++grp;
     }
+#endif
     __syncthreads();
     Partial cta = identity();
     if (threadIdx.x < 32) {

@@ -93,6 +93,9 @@ constexpr int kDynTiles = 1024;   // tile-partial slots per CTA (32 KB of shared
 #define FSB_DYN_MIN_GROUPS 4
 #endif
 constexpr unsigned kDynMinGroups = FSB_DYN_MIN_GROUPS;  // minimum 32-pair groups per claimed tile
+#ifndef FSB_DYN_PIPE
+#define FSB_DYN_PIPE 0  // experiment: register double-buffered groups in the claimed-tile kernel
+#endif
 #ifndef FSB_DYN_STRIPED
 #define FSB_DYN_STRIPED 1  // claimed tiles are stripes dealt round-robin to the CTAs (one front); 0: one contiguous chunk per CTA
 #endif

@@ -65,6 +65,12 @@ VARIANTS = {
     "d576x2": ["-DFSB_DYN_THREADS=576", "-DFSB_DYN_MIN_BLOCKS=2"],
     "d384x3": ["-DFSB_DYN_THREADS=384", "-DFSB_DYN_MIN_BLOCKS=3"],
     "d640x2": ["-DFSB_DYN_THREADS=640", "-DFSB_DYN_MIN_BLOCKS=2"],
+    # claimed-tile kernel with the next group's loads issued before the current group's compute
+    "pipe768": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=768"],
+    "pipe640": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=640"],
+    "pipe896": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=896"],
+    "pipe1024": ["-DFSB_DYN_PIPE=1"],
+    "pipe512x2": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=384", "-DFSB_DYN_MIN_BLOCKS=2"],
     # claimed-tile kernel: one contiguous chunk per CTA instead of round-robin stripes
     "chunked": ["-DFSB_DYN_STRIPED=0"],
     # claimed-tile kernel: minimum 32-pair groups per tile
