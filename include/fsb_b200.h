@@ -90,6 +90,10 @@ enum fsb_strategy {
 #define FSB_FLAG_DYNAMIC_TILES 0x100u /* LDG step kernel: one 1024-thread CTA per SM whose warps claim tiles
                                         (default: dynamic from 3e6 fish per shard) */
 #define FSB_FLAG_FLAT_GRID 0x200u   /* FSB_STRATEGY_GRID without thread-block clusters (one counter barrier) */
+#define FSB_FLAG_HOST_EXCHANGE 0x400u /* world_size > 1 without NCCL: the caller moves the 4-scalar rank
+                                        partials between move and eat (fsb_engine_partial /
+                                        fsb_engine_set_partials), e.g. over its own MPI or gloo
+                                        communicator; phase API only (run/simulate need NCCL or peers) */
 #define FSB_FLAG_CHECKED 0x40u     /* always evaluate the fp64 fast-path operand guards (default: elided
                                       while config and state are provably in range; results identical) */
 
@@ -203,6 +207,17 @@ int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta);
  * A single rank connects to itself at creation. */
 int fsb_engine_peer_handle(fsb_engine* e, void* out, size_t len);
 int fsb_engine_peer_connect(fsb_engine* e, const void* handles, size_t len);
+
+/* Host exchange (FSB_FLAG_HOST_EXCHANGE): the exchange step of eat_phase's
+ * max (sim.hpp:110-114 -> executor.hpp:83-103), made explicit for callers
+ * that bring their own communicator.  After fsb_engine_move, read this rank's
+ * partial {max(prev-cur), sum x*f, sum y*f, sum f} (out[4]), all-gather the
+ * world_size partials in rank order, and hand them back (parts[4*world_size])
+ * before fsb_engine_eat / fsb_engine_barycentre, which combine them in rank
+ * order on the device exactly as the NCCL path does.  Eat without a fresh
+ * set_partials fails with FSB_ERR_INVALID_ARGUMENT. */
+int fsb_engine_partial(fsb_engine* e, double out[4]);
+int fsb_engine_set_partials(fsb_engine* e, const double* parts, size_t count);
 
 /* Device self-test of the guarded fast fp64 paths the step kernel uses
  * (fsb_math.cuh): n generated operands (raw bit patterns incl. NaN, inf,

@@ -34,6 +34,7 @@ FLAG_CHECKED = 0x40
 FLAG_STATIC_TILES = 0x80
 FLAG_DYNAMIC_TILES = 0x100
 FLAG_FLAT_GRID = 0x200
+FLAG_HOST_EXCHANGE = 0x400
 
 
 class fsb_sim_config(ctypes.Structure):
@@ -98,6 +99,8 @@ SIGNATURES = [
     ("fsb_engine_last_launches", _int, [_vp, _P(_u64)]),
     ("fsb_engine_set_grid", _int, [_vp, _int]),
     ("fsb_engine_grid", _int, [_vp, _P(_int), _P(_int)]),
+    ("fsb_engine_partial", _int, [_vp, _vp]),
+    ("fsb_engine_set_partials", _int, [_vp, _vp, _sz]),
     ("fsb_engine_peer_handle", _int, [_vp, _vp, _sz]),
     ("fsb_engine_peer_connect", _int, [_vp, _vp, _sz]),
     ("fsb_selftest_fast_math", _int, [_int, _u64, _u64, _vp]),

@@ -126,6 +126,8 @@ struct fsb_engine {
     int device = 0;
     int rank = 0;
     int world = 1;
+    bool host_xchg = false;   // FSB_FLAG_HOST_EXCHANGE: the caller gathers the rank partials
+    bool xchg_ready = true;   // host exchange: every rank's partial of the current state is set
     int strategy = FSB_STRATEGY_AUTO;
     unsigned flags = 0;
     bool use_nccl = false;
@@ -256,6 +258,22 @@ fsb_dev::PeerXchg px_of(const fsb_engine* e, const uint64_t* seq_ptr, uint64_t i
 int need_peers(const fsb_engine* e) {
     if (e->peer_mode && !e->peer_connected)
         return fail(FSB_ERR_INVALID_ARGUMENT, "peer exchange not connected (fsb_engine_peer_connect)");
+    return FSB_OK;
+}
+
+// Host exchange with more than one rank: the caller's partials must be in place.
+bool host_multi(const fsb_engine* e) { return e->host_xchg && e->world > 1; }
+
+int need_partials(const fsb_engine* e) {
+    if (host_multi(e) && !e->xchg_ready)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "host exchange: fsb_engine_set_partials before eat/barycentre");
+    return FSB_OK;
+}
+
+int phase_only(const fsb_engine* e, const char* what) {
+    if (host_multi(e))
+        return fail(FSB_ERR_UNSUPPORTED, std::string("host exchange: ") + what +
+                                             " needs a per-step exchange (NCCL or peer); use move/eat");
     return FSB_OK;
 }
 
@@ -522,6 +540,7 @@ int reduce_current(fsb_engine* e) {
     TRY(exchange(e, 0));
     e->cur_buf = 0;
     e->max_valid = e->sums_valid = true;
+    e->xchg_ready = !host_multi(e);
     e->xseq += 1;
     return FSB_OK;
 }
@@ -697,7 +716,8 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     e->strategy = o.strategy;
     e->flags = o.flags;
     e->peer_mode = (o.flags & FSB_FLAG_PEER_EXCHANGE) != 0;
-    e->use_nccl = !e->peer_mode && (o.world_size > 1 || (o.flags & FSB_FLAG_FORCE_NCCL));
+    e->host_xchg = !e->peer_mode && (o.flags & FSB_FLAG_HOST_EXCHANGE) != 0;
+    e->use_nccl = !e->peer_mode && !e->host_xchg && (o.world_size > 1 || (o.flags & FSB_FLAG_FORCE_NCCL));
     fsb_shard_range(cfg->num_fish, e->world, e->rank, &e->first, &e->count);
 
     auto bail = [&](int rc) {
@@ -913,6 +933,7 @@ int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
     TRY(elapsed(e, seconds));
     e->cur_explicit = false;
     e->max_valid = e->sums_valid = true;
+    e->xchg_ready = !host_multi(e);
     e->cur_buf = 0;
     e->xseq += 1;
     return FSB_OK;
@@ -923,6 +944,7 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     TRY(need_peers(e));
     CU(cudaEventRecord(e->ev0, e->stream));
     if (!e->max_valid) TRY(reduce_current(e));
+    TRY(need_partials(e));
     fsb_dev::EatArgs a{};
     a.s = canonical(e);
     a.k = scalars_of(e->cfg);
@@ -965,6 +987,7 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
                    fsb_timing* timing) {
     TRY(guard(e));
     TRY(need_peers(e));
+    TRY(phase_only(e, "fsb_engine_run"));
     if (timing) *timing = fsb_timing{0.0, 0.0, 0.0};
     if (num_steps == 0) return FSB_OK;
     double secs = 0.0;
@@ -1000,6 +1023,7 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
 
 int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* timing) {
     TRY(guard(e));
+    TRY(phase_only(e, "fsb_engine_simulate"));
     CU(cudaEventRecord(e->ev0, e->stream));
     TRY(fsb_engine_init(e));
     CU(cudaEventRecord(e->ev1, e->stream));
@@ -1014,6 +1038,7 @@ int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
     TRY(guard(e));
     TRY(need_peers(e));
     if (!e->max_valid || !e->sums_valid) TRY(reduce_current(e));
+    TRY(need_partials(e));
     Partial r;
     TRY(host_combine(e, &r));
     if (sums) {
@@ -1025,6 +1050,40 @@ int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
         xy[0] = r.sx / r.sf;
         xy[1] = r.sy / r.sf;
     }
+    return FSB_OK;
+}
+
+int fsb_engine_partial(fsb_engine* e, double out[4]) {
+    TRY(guard(e));
+    TRY(need_peers(e));
+    if (!out) return fail(FSB_ERR_INVALID_ARGUMENT, "null out");
+    if (!e->max_valid || !e->sums_valid) TRY(reduce_current(e));
+    Partial p;
+    CU(cudaMemcpyAsync(&p, local_part(e, e->cur_buf), sizeof p, cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    out[0] = p.best;
+    out[1] = p.sx;
+    out[2] = p.sy;
+    out[3] = p.sf;
+    return FSB_OK;
+}
+
+int fsb_engine_set_partials(fsb_engine* e, const double* parts, size_t count) {
+    TRY(guard(e));
+    if (!e->host_xchg) return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials needs FSB_FLAG_HOST_EXCHANGE");
+    if (!parts || count != 4 * (size_t)e->world)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: need 4 * world_size doubles");
+    if (!e->max_valid || !e->sums_valid)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: no partial of the current state (fsb_engine_partial)");
+    // this rank's own entry must be its partial, bit for bit: catches partials out of rank order
+    double mine[4];
+    TRY(fsb_engine_partial(e, mine));
+    if (std::memcmp(mine, parts + 4 * (size_t)e->rank, sizeof mine) != 0)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: entry [rank] is not this rank's partial");
+    CU(cudaMemcpyAsync(all_part(e, e->cur_buf), parts, 4 * (size_t)e->world * sizeof(double),
+                       cudaMemcpyHostToDevice, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    e->xchg_ready = true;
     return FSB_OK;
 }
 
@@ -1082,6 +1141,7 @@ int fsb_engine_stream(fsb_engine* e, void** stream) {
 int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* kernel_ms) {
     TRY(guard(e));
     TRY(need_peers(e));
+    TRY(phase_only(e, "fsb_engine_time_step_kernels"));
     if (!kernel_ms && num_steps) return fail(FSB_ERR_INVALID_ARGUMENT, "null kernel_ms");
     if (e->count == 0 && e->world == 1) {
         for (uint64_t k = 0; k < num_steps; ++k) kernel_ms[k] = 0.0;
