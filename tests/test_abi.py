@@ -47,6 +47,16 @@ def test_built_for_sm100a_only():
     assert "sm_90" not in out and "sm_80" not in out
 
 
+def test_flag_constants_match_header():
+    """Every FSB_FLAG_* / FSB_STRATEGY_* value the Python layer passes equals the header's."""
+    src = open(HEADER).read()
+    flags = {m.group(1): int(m.group(2), 16) for m in re.finditer(r"#define FSB_(FLAG_\w+)\s+(0x[0-9a-fA-F]+)u", src)}
+    assert len(flags) >= 11 and "FLAG_HOST_EXCHANGE" in flags
+    for name, value in flags.items():
+        assert getattr(N, name) == value, name
+    assert len(set(flags.values())) == len(flags), "two flags share a bit"
+
+
 def test_abi_version():
     assert fsb.lib().fsb_abi_version() == 1
 
