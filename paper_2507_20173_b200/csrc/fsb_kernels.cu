@@ -519,11 +519,10 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
         uint64_t qs[kPairsPerThread], gi[kPairsPerThread];
 #pragma unroll
         for (int u = 0; u < kPairsPerThread; ++u) {
-            const uint64_t qq = base + (uint64_t)u * kStepThreads;
-            const uint64_t q = FSB_MEM_WINDOW ? lo + ((qq - lo) % FSB_MEM_WINDOW) : qq;
+            const uint64_t q = base + (uint64_t)u * kStepThreads;
             qs[u] = q;
-            gi[u] = a.gfirst + 2 * qq;
-            valid[u] = qq < hi;
+            gi[u] = a.gfirst + 2 * q;
+            valid[u] = q < hi;
             if (valid[u]) {
                 X[u] = X2[q];
                 Y[u] = Y2[q];
@@ -581,7 +580,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(cons
 // claiming keeps every warp busy until the share is done.  The share is a set
 // of stripes of >= kDynMinGroups 32-pair groups dealt round-robin to the CTAs,
 // so all SMs stream one moving front of the arrays (0-3% faster at 1e7 fish
-// than one contiguous chunk per CTA, FSB_DYN_STRIPED=0; the memory-only probe
+// than one contiguous chunk per CTA; the memory-only probe
 // shows 3%, profiles/r04_memory_bound_probe.jsonl).  Each tile's partial is
 // accumulated in a fixed order by whichever warp takes it and stored in its own
 // slot, and the slots are folded in tile order, so the sums stay
@@ -592,7 +591,7 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     __shared__ Partial tile_part[kDynTiles];
     // tile bookkeeping lives in shared memory, not in registers: the hot loop
     // is at the 64-register limit of 1024-thread CTAs
-    __shared__ unsigned next_tile, s_glo, s_ghi, s_gpt, s_ntiles;
+    __shared__ unsigned next_tile, s_ghi, s_gpt, s_ntiles;
     const StepParams P = params_of(a.k);
     pdl_wait_and_release();
     const Partial prev = combine_prev(a.part_in, a.world, a.px);
@@ -607,33 +606,17 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     // balanced contiguous chunk of 32-pair groups (32-bit group indices: up
     // to 2^37 fish per shard); tiles of gpt groups
     const uint64_t ngroups_all = (npairs + 31) / 32;
-#if FSB_DYN_STRIPED
     // stripes of gpt groups dealt round-robin to the CTAs (tile k of this CTA
     // is stripe k * gridDim + blockIdx.x): every SM works on one moving front
     unsigned gpt = (unsigned)((ngroups_all + (uint64_t)gridDim.x * kDynTiles - 1) / ((uint64_t)gridDim.x * kDynTiles));
-    if (gpt < kDynMinGroups) gpt = kDynMinGroups;
+    if (gpt < kDynMinGroups) gpt = kDynMinGroups;  // claims + tile flushes amortised over >= kDynMinGroups groups
     const unsigned nstripes = (unsigned)((ngroups_all + gpt - 1) / gpt);
     if (threadIdx.x == 0) {
         next_tile = 0;
-        s_glo = 0;
         s_ghi = (unsigned)ngroups_all;
         s_gpt = gpt;
         s_ntiles = nstripes > blockIdx.x ? (nstripes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
     }
-#else
-    const unsigned g_lo = (unsigned)(ngroups_all * blockIdx.x / gridDim.x);
-    const unsigned g_hi = (unsigned)(ngroups_all * (blockIdx.x + 1) / gridDim.x);
-    const unsigned ngroups = g_hi - g_lo;
-    unsigned gpt = (ngroups + kDynTiles - 1) / kDynTiles;
-    if (gpt < kDynMinGroups) gpt = kDynMinGroups;  // claims + tile flushes amortised over >= kDynMinGroups groups
-    if (threadIdx.x == 0) {
-        next_tile = 0;
-        s_glo = g_lo;
-        s_ghi = g_hi;
-        s_gpt = gpt;
-        s_ntiles = gpt ? (ngroups + gpt - 1) / gpt : 0u;
-    }
-#endif
     __syncthreads();
 
     double2* X2 = reinterpret_cast<double2*>(a.s.x);
@@ -643,81 +626,6 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
     const SoA2 src{X2, Y2, W2, P2, C2};
     const unsigned lane = threadIdx.x & 31;
-#if FSB_DYN_PIPE
-    // experiment: register double-buffering -- the next group's loads (claiming
-    // its tile early when the current one ends) are issued before the current
-    // group is computed, so every warp keeps one group in flight while it
-    // computes.  Costs 16-20 registers per thread: fewer, fatter threads per SM.
-    auto claim = [&](unsigned& t_, unsigned& g_, unsigned& e_) -> bool {
-        unsigned c = 0;
-        if (lane == 0) c = atomicAdd(&next_tile, 1u);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        const unsigned nt = *(volatile unsigned*)&s_ntiles;
-        if (c >= nt) return false;
-        t_ = rev ? nt - 1 - c : c;
-        const unsigned gpt_ = *(volatile unsigned*)&s_gpt;
-        const unsigned gh = *(volatile unsigned*)&s_ghi;
-#if FSB_DYN_STRIPED
-        g_ = (t_ * gridDim.x + blockIdx.x) * gpt_;
-#else
-        g_ = *(volatile unsigned*)&s_glo + t_ * gpt_;
-#endif
-        e_ = (g_ + gpt_ < gh) ? g_ + gpt_ : gh;
-        return true;
-    };
-    unsigned tile = 0, grp = 0, gend = 0;
-    bool have = claim(tile, grp, gend);
-    Partial acc = identity();
-    double2 X[1], Y[1], W[1], Q[1], C[1];
-    {
-        const uint64_t q = (uint64_t)grp * 32 + lane;
-        if (have && q < npairs) {
-            X[0] = X2[q];
-            Y[0] = Y2[q];
-            W[0] = W2[q];
-            Q[0] = P2[q];
-            if (kExplicitCur) C[0] = C2[q];
-        }
-    }
-    while (have) {
-        unsigned ntile = tile, ngrp = grp + 1, ngend = gend;
-        bool nhave = true;
-        if (ngrp == gend) nhave = claim(ntile, ngrp, ngend);
-        double2 NX, NY, NW, NQ, NC;
-        const uint64_t nq = (uint64_t)ngrp * 32 + lane;
-        if (nhave && nq < npairs) {
-            NX = X2[nq];
-            NY = Y2[nq];
-            NW = W2[nq];
-            NQ = P2[nq];
-            if (kExplicitCur) NC = C2[nq];
-        }
-        const uint64_t q = (uint64_t)grp * 32 + lane;
-        const bool valid[1] = {q < npairs};
-        const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
-        fused_pairs<kExplicitCur, 1, kSane, true>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
-        if (valid[0]) {
-            X2[q] = X[0];
-            Y2[q] = Y[0];
-            W2[q] = W[0];
-            P2[q] = Q[0];
-        }
-        if (!nhave || ntile != tile) {
-            const Partial tp = warp_reduce(acc);
-            if (lane == 0) tile_part[tile] = tp;
-            acc = identity();
-        }
-        X[0] = NX;
-        Y[0] = NY;
-        W[0] = NW;
-        Q[0] = NQ;
-        if (kExplicitCur) C[0] = NC;
-        tile = ntile;
-        grp = ngrp;
-        gend = ngend;
-        have = nhave;
-    }
-#else
     // one loop over groups; a warp claims its next tile when the current one
     // is exhausted (warp-uniform branch), flushing the finished tile's partial
     unsigned grp = 0, gend = 0, tile = ~0u;
@@ -738,11 +646,7 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
             FSB_CHECK(nt <= (unsigned)kDynTiles && tile < nt);
             const unsigned gpt_ = *(volatile unsigned*)&s_gpt;
             const unsigned gh = *(volatile unsigned*)&s_ghi;
-#if FSB_DYN_STRIPED
             grp = (tile * gridDim.x + blockIdx.x) * gpt_;
-#else
-            grp = *(volatile unsigned*)&s_glo + tile * gpt_;
-#endif
             gend = (grp + gpt_ < gh) ? grp + gpt_ : gh;
         }
         const uint64_t q = (uint64_t)grp * 32 + lane;
@@ -765,7 +669,6 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
         }
         ++grp;
     }
-#endif
     __syncthreads();
     Partial cta = identity();
     if (threadIdx.x < 32) {
@@ -802,10 +705,6 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
     __shared__ Partial scratch[32];
     __shared__ Partial shared_prev;
     Partial prev = identity();  // no pending eat at the start of a run
-#if FSB_GRID_TIMING
-    unsigned long long ts_prev = 0;
-    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_prev));
-#endif
     for (uint64_t k = 0; k < g.num_steps; ++k) {
         const uint64_t step = g.first_step + k;
         const bool eat = prev.best > 0.0;
@@ -813,19 +712,6 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
         Partial acc = identity();
         step_chunk<false, kSane>(a, P, eat, M, step, acc);
         const Partial blk = block_reduce(acc, scratch);
-#if FSB_GRID_TIMING
-        unsigned long long ts0 = 0, ts1 = 0;
-        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
-#if FSB_GRID_TIMING == 2
-        // experiment: every CTA's chunk time of the last step and its SM
-        if (threadIdx.x == 0 && k + 1 == g.num_steps && blockIdx.x < g.num_steps) {
-            unsigned smid;
-            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            g.trace[blockIdx.x] = (double)(ts0 - ts_prev);
-            if (g.bary) g.bary[blockIdx.x] = (double)smid;
-        }
-#endif
-#endif
         // Grid exchange: publish the CTA partial into slot [k&1][b], arrive on
         // the monotonic counter, wait for all G arrivals of this step, then
         // EVERY CTA folds the G partials itself in index order (the same tree
@@ -839,9 +725,6 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
             red_add_release_gpu(g.gen, 1ull);
             const unsigned long long target = (k + 1) * (unsigned long long)gridDim.x;
             while (ld_acquire_gpu(g.gen) < target) __nanosleep(20);
-#if FSB_GRID_TIMING
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts1));
-#endif
         }
         __syncthreads();
         Partial t = identity();
@@ -852,27 +735,14 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
             if (blockIdx.x == 0) {
                 g.trace[k] = tot.best;
                 if (g.bary) {
-#if FSB_GRID_TIMING == 1
-                    // experiment: CTA 0's globaltimer after its chunk, after the
-                    // barrier and after the fold, in place of the barycentre sums
-                    unsigned long long ts2;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2));
-                    g.bary[3 * k + 0] = __longlong_as_double((long long)ts0);
-                    g.bary[3 * k + 1] = __longlong_as_double((long long)ts1);
-                    g.bary[3 * k + 2] = __longlong_as_double((long long)ts2);
-#elif FSB_GRID_TIMING == 0
                     g.bary[3 * k + 0] = tot.sx;
                     g.bary[3 * k + 1] = tot.sy;
                     g.bary[3 * k + 2] = tot.sf;
-#endif
                 }
             }
         }
         __syncthreads();
         prev = shared_prev;
-#if FSB_GRID_TIMING
-        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts_prev));
-#endif
         __syncthreads();  // shared_prev / scratch reuse by the next step
     }
     // trailing eat of the last step, on the fish this CTA itself updated
@@ -997,8 +867,6 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
     __syncthreads();
 
     auto sub_base = [&](uint64_t j) { return lo + (rev ? nsub - 1 - j : j) * (uint64_t)kBulkTilePairs; };
-    // experiment-only FSB_MEM_WINDOW folds the addresses into an L2 window
-    auto mem_of = [&](uint64_t b) { return FSB_MEM_WINDOW ? lo + ((b - lo) % FSB_MEM_WINDOW) : b; };
     Partial acc = identity();
     if (t >= kBulkCompute) {
         // Producer warp, elected lane.  Sub-tile j lives in stage j % kBulkStages:
@@ -1006,7 +874,6 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
         // into the stage (empty[s]), bulk-store the stage to HBM and, as soon as
         // the store has read the stage out, reuse it for sub-tile j + kBulkStages.
         if (t == kBulkCompute) {
-            auto mem = mem_of;
             auto load = [&](uint64_t j) {
                 const int s = (int)(j % kBulkStages);
                 const uint64_t base = sub_base(j);
@@ -1014,10 +881,10 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
                 const unsigned bytes = (unsigned)(cnt * sizeof(double2));
                 FSB_CHECK(base >= lo && cnt >= 1 && cnt <= (uint64_t)kBulkTilePairs);
                 mbar_expect_tx(&full[s], 4 * bytes);
-                bulk_load(stage[s].x, X2 + mem(base), bytes, &full[s]);
-                bulk_load(stage[s].y, Y2 + mem(base), bytes, &full[s]);
-                bulk_load(stage[s].w, W2 + mem(base), bytes, &full[s]);
-                bulk_load(stage[s].p, P2 + mem(base), bytes, &full[s]);
+                bulk_load(stage[s].x, X2 + base, bytes, &full[s]);
+                bulk_load(stage[s].y, Y2 + base, bytes, &full[s]);
+                bulk_load(stage[s].w, W2 + base, bytes, &full[s]);
+                bulk_load(stage[s].p, P2 + base, bytes, &full[s]);
             };
             for (uint64_t j = 0; j < nsub && j < (uint64_t)kBulkStages; ++j) load(j);
             for (uint64_t j = 0; j < nsub; ++j) {
@@ -1026,10 +893,10 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
                 const uint64_t base = sub_base(j);
                 const uint64_t cnt = (hi - base < (uint64_t)kBulkTilePairs) ? hi - base : (uint64_t)kBulkTilePairs;
                 const unsigned bytes = (unsigned)(cnt * sizeof(double2));
-                bulk_store(X2 + mem(base), stage[s].x, bytes);
-                bulk_store(Y2 + mem(base), stage[s].y, bytes);
-                bulk_store(W2 + mem(base), stage[s].w, bytes);
-                bulk_store(P2 + mem(base), stage[s].p, bytes);
+                bulk_store(X2 + base, stage[s].x, bytes);
+                bulk_store(Y2 + base, stage[s].y, bytes);
+                bulk_store(W2 + base, stage[s].w, bytes);
+                bulk_store(P2 + base, stage[s].p, bytes);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 if (j + kBulkStages < nsub) {
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1210,9 +1077,6 @@ constexpr int kMaxCluster = 16;
 #define FSB_CLUSTER_F 1
 #endif
 constexpr int kClusterF = FSB_CLUSTER_F;  // fish per thread of the persistent cluster kernel
-#ifndef FSB_CLUSTER_EXP
-#define FSB_CLUSTER_EXP 0  // experiment builds only (tools/variants.py cexp1 / cexp2): results are not the reference's
-#endif
 
 __device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem, unsigned rank) {
     uint32_t r;
@@ -1293,7 +1157,7 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     for (uint64_t k = 0; k < a.num_steps; ++k) {
         const uint64_t step = a.first_step + k;
         const unsigned b = (unsigned)(k & 1);
-        if (threadIdx.x == 0 && (FSB_CLUSTER_EXP == 0 || kBary))
+        if (threadIdx.x == 0)
             mbar_expect_tx(&xbar[b], ncta * kBytes);  // may race the pushes: fine
         const bool eat = M > 0.0;
         const SharedDivisor D = make_divisor(eat ? M : 1.0);
@@ -1313,26 +1177,6 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
                 }
             }
         }
-#if FSB_CLUSTER_EXP == 1  // experiment: warp-local max only (no block reduction, no exchange)
-        if (!kBary) {
-#pragma unroll
-            for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
-            M = warp_max_redux(acc.best);
-            if (crank == 0 && threadIdx.x == 0) a.trace[k] = M;
-            continue;
-        }
-#elif FSB_CLUSTER_EXP == 2  // experiment: block reduction, no cluster exchange
-        if (!kBary) {
-            const double bm = key_value(block_max_key(max_key(acc.best), scratch_key));
-#pragma unroll
-            for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
-            if (threadIdx.x == 0) slots[b][0].best = bm;
-            __syncthreads();
-            M = slots[b][0].best;
-            if (crank == 0 && threadIdx.x == 0) a.trace[k] = M;
-            continue;
-        }
-#endif
         Partial blk = identity();
         if (kBary) blk = block_reduce(acc, scratch);
         else  // the CTA max travels as its key (bits in .best), decoded after the fold
@@ -1451,10 +1295,6 @@ __device__ __forceinline__ void cgrid_leader_exchange(const CGridArgs& g, uint64
     const unsigned lane = threadIdx.x;
     const unsigned C = sreg_cluster_size(), cid = sreg_cluster_id(), NC = sreg_num_clusters();
     mbar_wait_cluster(&xbar[b], par);
-#if FSB_GRID_TIMING == 1 || FSB_GRID_TIMING == 3
-    unsigned long long tsx, tsf;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tsx));
-#endif
     const Partial cpart = warp_reduce(lane < C ? slots[b][lane] : identity());  // fixed butterfly
     // Cluster partials travel in self-validating slots: ring position k % 3,
     // one 128-B line per cluster, every word the SENTINEL until this step's
@@ -1494,16 +1334,6 @@ __device__ __forceinline__ void cgrid_leader_exchange(const CGridArgs& g, uint64
     __syncwarp();
     asm volatile("fence.acquire.gpu;" ::: "memory");  // L1 invalidate only, no MEMBAR
     t = warp_reduce(t);
-#if FSB_GRID_TIMING == 1 || FSB_GRID_TIMING == 3
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tsf));
-#endif
-#if FSB_GRID_TIMING == 3
-    // experiment: every leader's cluster-ready and global-done times of the last step
-    if (lane == 0 && k + 1 == g.num_steps && g.bary && 2 * cid + 1 < 3 * g.num_steps) {
-        g.bary[2 * cid + 0] = __longlong_as_double((long long)tsx);
-        g.bary[2 * cid + 1] = __longlong_as_double((long long)tsf);
-    }
-#endif
     if (lane < C) {
         const uint32_t dst = cluster_map(smem_u32(&tslot[b]), lane);
         const uint32_t bar = cluster_map(smem_u32(&tbar[b]), lane);
@@ -1513,15 +1343,9 @@ __device__ __forceinline__ void cgrid_leader_exchange(const CGridArgs& g, uint64
     if (cid == 0 && lane == 0) {
         g.trace[k] = t.best;
         if (g.bary) {
-#if FSB_GRID_TIMING == 1
-            // experiment: leader 0's globaltimer after the cluster wait and after the global fold
-            g.bary[3 * k + 1] = __longlong_as_double((long long)tsx);
-            g.bary[3 * k + 2] = __longlong_as_double((long long)tsf);
-#elif FSB_GRID_TIMING == 0
             g.bary[3 * k + 0] = t.sx;
             g.bary[3 * k + 1] = t.sy;
             g.bary[3 * k + 2] = t.sf;
-#endif
         }
     }
 }
@@ -1557,13 +1381,6 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(con
         Partial acc = identity();
         step_chunk<false, kSane>(a, P, eat, M, step, acc);
         const Partial blk = block_reduce(acc, scratch);  // every lane of warp 0 holds it
-#if FSB_GRID_TIMING == 1
-        if (blockIdx.x == 0 && threadIdx.x == 0 && g.bary) {  // experiment: CTA 0 after its chunk
-            unsigned long long ts0;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
-            g.bary[3 * k + 0] = __longlong_as_double((long long)ts0);
-        }
-#endif
         if (threadIdx.x == 0) {  // this CTA's partial into the leader's slot
             const uint32_t dst = cluster_map(smem_u32(&slots[b][sreg_cluster_rank()]), 0);
             const uint32_t bar = cluster_map(smem_u32(&xbar[b]), 0);

@@ -46,21 +46,10 @@ namespace fsb_dev {
 #define FSB_MIN_BLOCKS 4
 #endif
 
-// Experiment only (tools/variants.py "l2_*"): fold each CTA's memory indices
-// into its own window of FSB_MEM_WINDOW pairs so the step runs from L2 --
-// separates compute from DRAM time.  Results are meaningless with a window;
-// the product build keeps 0 (off).
-#ifndef FSB_MEM_WINDOW
-#define FSB_MEM_WINDOW 0
-#endif
-
 #ifndef FSB_CLUSTER_MIN_FISH
 #define FSB_CLUSTER_MIN_FISH 256  // persistent kernel: fish per CTA before adding CTAs
 #endif
 
-#ifndef FSB_GRID_TIMING
-#define FSB_GRID_TIMING 0  // experiment: grid kernel records CTA 0's phase timestamps in place of bary
-#endif
 #ifndef FSB_BULK_STAGES
 #define FSB_BULK_STAGES 4
 #endif
@@ -93,12 +82,6 @@ constexpr int kDynTiles = 1024;   // tile-partial slots per CTA (32 KB of shared
 #define FSB_DYN_MIN_GROUPS 4
 #endif
 constexpr unsigned kDynMinGroups = FSB_DYN_MIN_GROUPS;  // minimum 32-pair groups per claimed tile
-#ifndef FSB_DYN_PIPE
-#define FSB_DYN_PIPE 0  // experiment: register double-buffered groups in the claimed-tile kernel
-#endif
-#ifndef FSB_DYN_STRIPED
-#define FSB_DYN_STRIPED 1  // claimed tiles are stripes dealt round-robin to the CTAs (one front); 0: one contiguous chunk per CTA
-#endif
 constexpr int kTileFish = 2 * kTilePairs;
 
 // step_kernel_bulk: 8 compute warps x kBulkPairsPerThread pairs per sub-tile,

@@ -10,6 +10,17 @@ Experiments that lost and were removed from the sources after measurement
 stores, IMAD.HI shifts, one fish per thread) are in profiles/r0*_variants.jsonl;
 L2 evict_last carry-over and the cluster grid's predrawn RNG in
 profiles/r04_ab_session.jsonl.
+
+Instrumented experiment builds that are not product code were removed from
+csrc/fsb_kernels.cu in round 2 (their measurements stay in profiles/): the
+L2-window compute-only builds (FSB_MEM_WINDOW, profiles/r03_variants.jsonl),
+the grid kernels' globaltimer phase stamps (FSB_GRID_TIMING,
+profiles/r03_grid_phases.jsonl, r03_grid_ctas.jsonl, r03_cgrid_leaders.jsonl),
+the persistent kernel without its exchange (FSB_CLUSTER_EXP,
+profiles/r04_ab_session.jsonl), the register double-buffered claimed-tile
+kernel (FSB_DYN_PIPE, profiles/r05_ab_pipe.jsonl) and the contiguous-chunk
+claimed tiles (FSB_DYN_STRIPED=0).  Their sources are in git history at
+commit 7dc3518 (`git show 7dc3518:paper_2507_20173_b200/csrc/fsb_kernels.cu`).
 """
 from __future__ import annotations
 
@@ -37,16 +48,11 @@ VARIANTS = {
     "b1s4m3": ["-DFSB_BULK_PAIRS=1", "-DFSB_BULK_STAGES=4", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b2s2m3": ["-DFSB_BULK_PAIRS=2", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=3"],
     "b4s2m1": ["-DFSB_BULK_PAIRS=4", "-DFSB_BULK_STAGES=2", "-DFSB_BULK_MIN_BLOCKS=1"],
-    "l2_bulk": ["-DFSB_MEM_WINDOW=512"],
     # bulk ring with more compute warps per SM (compute threads x stages x CTAs per SM): all slower
     "bk992s3m1": ["-DFSB_BULK_COMPUTE=992", "-DFSB_BULK_STAGES=3", "-DFSB_BULK_MIN_BLOCKS=1"],
     # LDG kernel with bigger CTAs (fewer CTA partials in the per-step grid reduction)
     "t512b2": ["-DFSB_STEP_THREADS=512", "-DFSB_MIN_BLOCKS=2"],
     "t1024b1": ["-DFSB_STEP_THREADS=1024", "-DFSB_MIN_BLOCKS=1"],
-    # experiment: grid kernel phase timestamps (tools/grid_phases.py)
-    "gridtiming": ["-DFSB_GRID_TIMING=1"],
-    "gridcta": ["-DFSB_GRID_TIMING=2"],
-    "gridlead": ["-DFSB_GRID_TIMING=3"],
     # cluster-reduced grid kernel: CTAs per cluster
     "cg2": ["-DFSB_CGRID_CLUSTER=2"],
     "cg4": ["-DFSB_CGRID_CLUSTER=4"],
@@ -54,9 +60,6 @@ VARIANTS = {
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
-    # experiment: persistent cluster kernel without the exchange (1: warp max only, 2: block max only)
-    "cexp1": ["-DFSB_CLUSTER_EXP=1"],
-    "cexp2": ["-DFSB_CLUSTER_EXP=2"],
     # persistent cluster kernel: fish per thread
     "cf2": ["-DFSB_CLUSTER_F=2"],
     "cf2m512": ["-DFSB_CLUSTER_F=2", "-DFSB_CLUSTER_MIN_FISH=512"],
@@ -65,21 +68,10 @@ VARIANTS = {
     "d576x2": ["-DFSB_DYN_THREADS=576", "-DFSB_DYN_MIN_BLOCKS=2"],
     "d384x3": ["-DFSB_DYN_THREADS=384", "-DFSB_DYN_MIN_BLOCKS=3"],
     "d640x2": ["-DFSB_DYN_THREADS=640", "-DFSB_DYN_MIN_BLOCKS=2"],
-    # claimed-tile kernel with the next group's loads issued before the current group's compute
-    "pipe768": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=768"],
-    "pipe640": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=640"],
-    "pipe896": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=896"],
-    "pipe1024": ["-DFSB_DYN_PIPE=1"],
-    "pipe512x2": ["-DFSB_DYN_PIPE=1", "-DFSB_DYN_THREADS=384", "-DFSB_DYN_MIN_BLOCKS=2"],
-    # claimed-tile kernel: one contiguous chunk per CTA instead of round-robin stripes
-    "chunked": ["-DFSB_DYN_STRIPED=0"],
     # claimed-tile kernel: minimum 32-pair groups per tile
     "dg1": ["-DFSB_DYN_MIN_GROUPS=1"],
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
-    # experiment: LDG kernel with all memory folded into 8K pairs (compute-only time)
-    "l2_p1b4": ["-DFSB_PAIRS=1", "-DFSB_MIN_BLOCKS=4", "-DFSB_MEM_WINDOW=512"],
-    "l2_p4b2": ["-DFSB_PAIRS=4", "-DFSB_MIN_BLOCKS=2", "-DFSB_MEM_WINDOW=1024"],
 }
 
 
