@@ -6,10 +6,14 @@ A bench "step" is one simulation step over the whole school: swim + objective
 every fish.  Workload at N=1: BASELINE.json configs[1] =
 10,000,000 fish (fp64 SoA, 320 MB of state > 126 MB L2), the reference
 SimConfig mapping pond_size=200, weight_scale=1, step_base=0.1, seed=7.
-Multi-GPU (torchrun): weak scaling, 10^7 fish per GPU, contiguous shards, one
-NCCL allgather of 4 fp64 per step inside the CUDA graph.
+Multi-GPU (torchrun, N > 1) or --scaling: BASELINE configs[3]'s weak-scaling
+share, 1.25e8 fish per GPU (10^9 fish at N=8), contiguous shards, one NCCL
+allgather of 4 fp64 per step inside the CUDA graph.  The same record carries
+the N=1 point at that per-GPU size (rank 0's GPU alone, timed before the
+collective run) and the per-step cost of the NCCL and peer exchanges measured
+on one rank.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--scaling]
 
 `value` = fish-updates/s with the school resident in HBM (device events around
 exactly K steps, max over ranks).  `e2e` = the same metric through the C-ABI
@@ -29,7 +33,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FISH_PER_GPU = 10_000_000
+FISH_PER_GPU = 10_000_000   # BASELINE configs[1]: the single-GPU metric
+C3_SHARE = 125_000_000      # BASELINE configs[3] weak scaling: 1.25e8 per GPU, 1e9 fish at 8 GPUs
 BYTES_PER_UPDATE = 80  # read + write of the 5 x fp64 fish state
 MOVED_BYTES_PER_UPDATE = 64  # this design: read + write of x, y, w, prev (cur recomputed)
 METRIC = "fish-updates/sec (fish x steps / s)"
@@ -173,10 +178,31 @@ def cpu_baseline_sample(n: int, steps: int):
     }
 
 
+def fish_per_gpu(args, world: int) -> int:
+    """configs[1] (1e7) for the single-GPU metric; the configs[3] weak-scaling
+    share (1.25e8 per GPU) under torchrun with N > 1 or with --scaling."""
+    if args.fish:
+        return args.fish
+    return C3_SHARE if (world > 1 or args.scaling) else FISH_PER_GPU
+
+
 def workload(n_per_gpu: int, world: int) -> str:
     """The config.workload string both arms print (the driver pairs them)."""
+    if n_per_gpu == FISH_PER_GPU:
+        which = "BASELINE configs[1]"
+    elif n_per_gpu == C3_SHARE:
+        which = "BASELINE configs[3] weak-scaling share, 1e9 fish at 8 GPUs"
+    else:
+        which = "custom size"
     return (f"FSB {n_per_gpu} fish per GPU fp64 SoA, pond 200, w0 1.0, step_base 0.1, "
-            f"seed 7 (BASELINE configs[1]); {n_per_gpu * world} fish total")
+            f"seed 7 ({which}); {n_per_gpu * world} fish total")
+
+
+def common_config(n_local: int, world: int) -> dict:
+    """The config dict both arms print, key for key; arm-specific details go
+    to the sibling key "arm"."""
+    return {"workload": workload(n_local, world), "fish_per_gpu": n_local, "fish_total": n_local * world,
+            "pond_size": 200.0, "weight_scale": 1.0, "step_base": 0.1, "seed": 7}
 
 
 def run_reference(args, world, rank):
@@ -188,7 +214,7 @@ def run_reference(args, world, rank):
     import oracle
 
     threads = os.cpu_count() or 1
-    n = args.fish
+    n = fish_per_gpu(args, world)
     cfg = oracle.baseline_config(n, args.warmup + args.steps)
     ref = oracle.Reference()
     total, per, _ = ref.time_steps(cfg, warmup=args.warmup, steps=args.steps, threads=threads,
@@ -211,8 +237,10 @@ def run_reference(args, world, rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (reference init_school, seed 7)",
-        "config": {"workload": workload(n, world), "fish": n, "parallelism": f"cpu {threads} threads",
-                   "sample": f"{n} fish (the per-GPU school) on the host"},
+        "config": common_config(n, world),
+        "arm": {"parallelism": f"cpu {threads} threads", "construct": "reference default RunConfig",
+                "sample": f"{n} fish (the per-GPU school) on the host, the bounded sample of the "
+                          f"{n * world}-fish workload"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -286,6 +314,46 @@ def same_bytes_memory_bound(state_bytes: int, device: int):
     return out
 
 
+def time_one_rank(n: int, steps: int, warmup: int, device: int, **kw):
+    """One world-1 engine at n fish on this GPU: device time of `steps` steps
+    after `warmup` (graph of step kernels; the same run() the bench times)."""
+    import paper_2507_20173_b200 as fsb
+
+    cfg = fsb.baseline_config(n, warmup + steps)
+    with fsb.Engine(cfg, device=device, **kw) as eng:
+        eng.init()
+        eng.run(0, warmup)
+        _, _, t = eng.run(warmup, steps)
+        return t.seconds_loop, t.seconds_eat
+
+
+def scaling_points(n_local: int, args, device: int):
+    """Rank 0, before the collective run: the N=1 point at the same per-GPU
+    size, and the per-step cost of each exchange measured on one rank (the
+    in-graph NCCL allgather, the peer-window stores of the step kernel) as the
+    difference to the plain single-rank graph."""
+    import paper_2507_20173_b200 as fsb
+
+    plain, plain_eat = time_one_rank(n_local, args.steps, args.warmup, device, strategy="stream")
+    nccl, nccl_eat = time_one_rank(n_local, args.steps, args.warmup, device, strategy="stream", force_nccl=True,
+                                   nccl_unique_id=fsb.nccl_unique_id())
+    peer, peer_eat = time_one_rank(n_local, args.steps, args.warmup, device, strategy="stream", peer=True)
+    k = args.steps
+    return {
+        "n1_value": n_local * k / plain,
+        "n1_ms_per_step": 1e3 * plain / k,
+        "n1_fish": n_local,
+        "exchange_us_per_step_one_rank": {
+            "nccl_allgather": 1e6 * (nccl - plain) / k,
+            "peer_window": 1e6 * (peer - plain) / k,
+        },
+        "eat_region_us_per_step_one_rank": {"plain": 1e6 * plain_eat / k, "nccl_allgather": 1e6 * nccl_eat / k,
+                                            "peer_window": 1e6 * peer_eat / k},
+        "note": "rank 0's GPU alone, before the collective run; exchange cost = the graph with the exchange "
+                "minus the plain graph, on one rank (the N>1 run adds the NVLink transfer)",
+    }
+
+
 def run_ours(args, world, rank, local):
     import ctypes
 
@@ -294,8 +362,12 @@ def run_ours(args, world, rank, local):
     import paper_2507_20173_b200 as fsb
     from paper_2507_20173_b200 import _native as N
 
-    n_local = args.fish
+    n_local = fish_per_gpu(args, world)
     n_total = n_local * world
+    scaling = None
+    if (world > 1 or args.scaling) and rank == 0 and not args.no_scaling_points:
+        scaling = scaling_points(n_local, args, local)
+    barrier(world)
     cfg = fsb.baseline_config(n_total, args.warmup + args.steps)
     uid = None
     if world > 1 and not args.peer:
@@ -324,8 +396,10 @@ def run_ours(args, world, rank, local):
         trace, _, timing = eng.run(args.warmup, args.steps)
     eng.synchronize()
     barrier(world)
-    t_dev = allreduce_max(world, timing.seconds_move, local)
+    t_dev = allreduce_max(world, timing.seconds_loop, local)
+    t_eat = allreduce_max(world, timing.seconds_eat, local)
     launches = eng.last_launches()
+    strategy_used, fallback = eng.last_strategy()
     value = n_total * args.steps / t_dev
 
     # per-kernel durations of the fused step kernel (events on the engine stream)
@@ -366,13 +440,14 @@ def run_ours(args, world, rank, local):
             "h2d_bytes_per_step": nbytes / args.steps,
             "d2h_bytes_per_step": (nbytes + 8 * args.steps) / args.steps,
             "upload_ms": 1e3 * (t1 - t0), "run_ms": 1e3 * (t2 - t1), "download_ms": 1e3 * (t3 - t2),
-            "note": "per rank: AoS School upload from pinned host memory + K steps + trace and "
-                    "School download, wall clock, max over ranks",
+            "note": f"per rank: AoS School upload from pinned host memory + K={args.steps} steps + trace and "
+                    "School download, wall clock, max over ranks; the school crosses PCIe once each way per "
+                    "call, so e2e grows with K (the per-step bytes shrink as 1/K)",
         }
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_sample(args.fish, args.cpu_steps)
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_sample(min(n_local, FISH_PER_GPU), args.cpu_steps)
 
     if rank == 0:
         line = {
@@ -388,15 +463,18 @@ def run_ours(args, world, rank, local):
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (reference init_school on device, seed 7)",
-            "config": {
-                "workload": workload(n_local, world),
-                "fish_per_gpu": n_local,
-                "fish_total": n_total,
+            "config": common_config(n_local, world),
+            "arm": {
                 "parallelism": f"fish-sharded x{world}" + (" + NCCL allgather(4 fp64)/step" if world > 1 else ""),
                 "strategy": args.strategy,
+                "strategy_used": strategy_used,
+                "fallback": fallback,
                 "l2": f"inputs larger than L2 ({n_local * 32 / 1e6:.0f} MB resident state vs 126 MB L2)",
                 "timed": "K fused step kernels + 1 trailing eat kernel, one CUDA graph launch",
             },
+            "eat_region": {"seconds": t_eat, "us_per_step": 1e6 * t_eat / args.steps,
+                           "note": "SimResult::seconds_eat on the device: from every fish of a step updated to "
+                                   "the next kernel holding the global max (max over ranks)"},
             "roofline": {
                 "bound": "hbm",
                 "kernel": kernel,
@@ -426,6 +504,8 @@ def run_ours(args, world, rank, local):
             "clocks": clk.summary(),
             "trace_last": float(trace[-1]),
         }
+        if scaling:
+            line["scaling_points"] = scaling
         print(json.dumps(line), flush=True)
     eng.close()
 
@@ -436,7 +516,13 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--fish", type=int, default=FISH_PER_GPU, help="fish per GPU")
+    ap.add_argument("--fish", type=int, default=0,
+                    help="fish per GPU (default: 1e7 = configs[1]; 1.25e8 = the configs[3] share for N > 1)")
+    ap.add_argument("--scaling", action="store_true",
+                    help="the weak-scaling workload (1.25e8 fish per GPU) even at N=1, with the N=1 point "
+                         "and the one-rank exchange costs in the record")
+    ap.add_argument("--no-scaling-points", action="store_true",
+                    help="skip the N=1 point and exchange costs measured before an N>1 / --scaling run")
     ap.add_argument("--strategy", default="auto", choices=["auto", "stream", "persistent"])
     ap.add_argument("--no-alternate", action="store_true",
                     help="fixed tile order (default reverses odd steps to reuse L2 across steps)")

@@ -48,7 +48,7 @@ int main(int argc, char** argv) {
                     engines[r] = std::make_unique<fsb::gpu::Engine>(cfg, o);  // collective NCCL init
                     engines[r]->init();
                     const fsb_timing t = engines[r]->run(0, cfg.num_steps, traces[r]);
-                    seconds[r] = t.seconds_move;
+                    seconds[r] = t.seconds_loop;
                 } catch (const std::exception& e) {
                     errors[r] = e.what();
                 }

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define FSB_B200_ABI_VERSION 1
+#define FSB_B200_ABI_VERSION 2
 
 /* Status codes.  fsb_last_error() holds a message for the calling thread. */
 enum fsb_status {
@@ -59,11 +59,21 @@ typedef struct fsb_fish {
     double current_objective;
 } fsb_fish;
 
-/* fsb::SimResult timing fields (sim.hpp:128-130), device-timed (cudaEvent). */
+/* fsb::SimResult timing fields (sim.hpp:125-131), device-timed.
+ * seconds_eat is the reference's eat-region time: the global max only
+ * (sim.hpp:103,112 -- the weight update is not timed there either).  The max
+ * is fused into the step kernels, so it is measured on the device with
+ * %globaltimer where it sits on the critical path: per step, from the moment
+ * every fish of the step has been updated to the moment the kernel that
+ * needs the global max holds it (CTA and grid reductions, the kernel boundary
+ * or in-kernel grid barrier, the NCCL / peer exchange).  For the persistent
+ * strategies it is the mean over CTAs of each CTA's time from its own fish
+ * done to holding the max.  seconds_move = seconds_loop - seconds_eat. */
 typedef struct fsb_timing {
-    double seconds_total; /* init + step loop (simulate) or the step loop (run) */
-    double seconds_move;  /* step loop: fused move+max(+deferred eat) kernels   */
-    double seconds_eat;   /* standalone eat kernels (trailing / phase eat)      */
+    double seconds_total; /* init + step loop (simulate) or the step loop (run), cudaEvent */
+    double seconds_move;  /* the step loop outside the eat region                        */
+    double seconds_eat;   /* the eat region: the global max only (see above)             */
+    double seconds_loop;  /* the step loop, cudaEvent (what the bench divides by)        */
 } fsb_timing;
 
 /* Step-loop strategies. */
@@ -72,9 +82,11 @@ enum fsb_strategy {
                                     else stream */
     FSB_STRATEGY_STREAM = 1,     /* one fused step kernel per step, CUDA-graph replayed  */
     FSB_STRATEGY_PERSISTENT = 2, /* one thread-block cluster runs all steps on chip       */
-    FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps; CTAs
-                                    reduce inside thread-block clusters, cluster leaders meet through
-                                    one global slot each (single GPU, mid-size schools) */
+    FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps (single GPU,
+                                    mid-size schools): up to ~1.06e6 fish the school lives in shared
+                                    memory (one CTA per SM, every CTA polls every CTA's slot); larger
+                                    schools stay in L2, CTAs reduce inside thread-block clusters and
+                                    cluster leaders meet through one global slot each */
 };
 
 /* Engine flags. */
@@ -94,6 +106,9 @@ enum fsb_strategy {
                                         partials between move and eat (fsb_engine_partial /
                                         fsb_engine_set_partials), e.g. over its own MPI or gloo
                                         communicator; phase API only (run/simulate need NCCL or peers) */
+#define FSB_FLAG_L2_GRID 0x800u     /* FSB_STRATEGY_GRID: keep the school in L2/HBM (cluster-reduced grid)
+                                      even when it fits in shared memory (default: on chip up to ~1.06e6
+                                      fish, one CTA per SM holding its pairs for all steps) */
 #define FSB_FLAG_CHECKED 0x40u     /* always evaluate the fp64 fast-path operand guards (default: elided
                                       while config and state are provably in range; results identical) */
 
@@ -152,11 +167,18 @@ int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count);
 int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds);
 
 /* eat_phase(school, cfg, exec) (sim.hpp:110-123): global max of prev-cur
- * (-inf for an empty school) and the weight update when it is > 0. */
+ * (-inf for an empty school) and the weight update when it is > 0.
+ * seconds: EatResult::seconds, the max only (sim.hpp:103): the reduction tail
+ * of the preceding move kernel plus this call's combine, device-timed. */
 int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds);
 
 /* The step loop of simulate (sim.hpp:139-144) for steps
  * [first_step, first_step + num_steps): T x (move, eat), on device.
+ * Strategy AUTO: the persistent cluster kernel up to 16,384 fish, the
+ * cooperative grid up to 2.5e6, else the graph of step kernels; if the device
+ * refuses the co-resident launch the run falls back to the graph (see
+ * fsb_engine_last_strategy).  An explicit PERSISTENT / GRID request fails
+ * with FSB_ERR_UNSUPPORTED instead.
  * trace[num_steps] receives max_diff per step (EatResult::max_diff);
  * bary[3*num_steps] (may be NULL) the per-step sums {sum x*f, sum y*f, sum f}
  * over all shards.  timing may be NULL. */
@@ -191,6 +213,13 @@ int fsb_engine_time_step_kernels(fsb_engine* e, uint64_t first_step, uint64_t nu
 /* Kernel launch count of the last fsb_engine_run (for bench accounting). */
 int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches);
 
+/* The step-loop strategy the last fsb_engine_run executed (enum fsb_strategy;
+ * never AUTO) and, when an AUTO run had to leave its first choice because the
+ * device refused to co-schedule the persistent grid or cluster (a profiler
+ * replay, MPS, a shared device), the launch error that made it fall back to
+ * the graph of step kernels ("" otherwise).  The string lives until the next run. */
+int fsb_engine_last_strategy(const fsb_engine* e, int* strategy, const char** fallback_reason);
+
 /* Configuration sweeps (the GPU analogue of the reference's thread-count
  * experiments, bench.hpp:79-148): set the CTA count of the compact-state step
  * and eat kernels (ctas = 0 restores the automatic SMs x occupancy grid).  Each
@@ -211,12 +240,15 @@ int fsb_engine_peer_connect(fsb_engine* e, const void* handles, size_t len);
 /* Host exchange (FSB_FLAG_HOST_EXCHANGE): the exchange step of eat_phase's
  * max (sim.hpp:110-114 -> executor.hpp:83-103), made explicit for callers
  * that bring their own communicator.  After fsb_engine_move, read this rank's
- * partial {max(prev-cur), sum x*f, sum y*f, sum f} (out[4]), all-gather the
- * world_size partials in rank order, and hand them back (parts[4*world_size])
- * before fsb_engine_eat / fsb_engine_barycentre, which combine them in rank
- * order on the device exactly as the NCCL path does.  Eat without a fresh
- * set_partials fails with FSB_ERR_INVALID_ARGUMENT. */
-int fsb_engine_partial(fsb_engine* e, double out[4]);
+ * partial {max(prev-cur), sum x*f, sum y*f, sum f, epoch} (out[5]; epoch =
+ * the exchange sequence number, equal on every rank at the same step),
+ * all-gather the world_size partials in rank order, and hand them back
+ * (parts[5*world_size]) before fsb_engine_eat / fsb_engine_barycentre, which
+ * combine them in rank order on the device exactly as the NCCL path does.
+ * set_partials rejects a set whose entry [rank] is not this rank's partial or
+ * whose epochs differ (a rank that moved twice or skipped a move).  Eat
+ * without a fresh set_partials fails with FSB_ERR_INVALID_ARGUMENT. */
+int fsb_engine_partial(fsb_engine* e, double out[5]);
 int fsb_engine_set_partials(fsb_engine* e, const double* parts, size_t count);
 
 /* Device self-test of the guarded fast fp64 paths the step kernel uses

@@ -35,6 +35,7 @@ FLAG_STATIC_TILES = 0x80
 FLAG_DYNAMIC_TILES = 0x100
 FLAG_FLAT_GRID = 0x200
 FLAG_HOST_EXCHANGE = 0x400
+FLAG_L2_GRID = 0x800
 
 
 class fsb_sim_config(ctypes.Structure):
@@ -53,6 +54,7 @@ class fsb_timing(ctypes.Structure):
         ("seconds_total", ctypes.c_double),
         ("seconds_move", ctypes.c_double),
         ("seconds_eat", ctypes.c_double),
+        ("seconds_loop", ctypes.c_double),
     ]
 
 
@@ -97,6 +99,7 @@ SIGNATURES = [
     ("fsb_engine_stream", _int, [_vp, _P(_vp)]),
     ("fsb_engine_time_step_kernels", _int, [_vp, _u64, _u64, _vp]),
     ("fsb_engine_last_launches", _int, [_vp, _P(_u64)]),
+    ("fsb_engine_last_strategy", _int, [_vp, _P(_int), _P(ctypes.c_char_p)]),
     ("fsb_engine_set_grid", _int, [_vp, _int]),
     ("fsb_engine_grid", _int, [_vp, _P(_int), _P(_int)]),
     ("fsb_engine_partial", _int, [_vp, _vp]),
@@ -105,6 +108,9 @@ SIGNATURES = [
     ("fsb_engine_peer_connect", _int, [_vp, _vp, _sz]),
     ("fsb_selftest_fast_math", _int, [_int, _u64, _u64, _vp]),
 ]
+
+
+ABI_VERSION = 2  # FSB_B200_ABI_VERSION
 
 
 class FsbError(RuntimeError):
@@ -147,7 +153,7 @@ def lib() -> ctypes.CDLL:
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
-        if L.fsb_abi_version() != 1:
+        if L.fsb_abi_version() != ABI_VERSION:
             raise ImportError("libfsb_b200.so ABI mismatch")
         _lib = L
     return _lib

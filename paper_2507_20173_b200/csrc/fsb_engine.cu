@@ -164,6 +164,9 @@ struct fsb_engine {
     int cgrid_nc = 0;                        // co-resident clusters of the cluster-reduced grid kernel (0: none)
     double* d_cl_slots = nullptr;            // [kSlotRing][cgrid_nc][kSlotWords]
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
+    unsigned sg_cap = 0;     // shared-memory-resident grid: fish pairs per CTA (0: unavailable)
+    int sg_grid = 0;         // ... its CTAs (one per SM)
+    unsigned long long* d_sg_keys = nullptr;  // [3] per-step max keys of the shared-memory grid
 
     void* staging = nullptr;  // device AoS staging (two halves of kStagingFish / 2 fish: double-buffered transfers)
     cudaStream_t xfer = nullptr;        // copy stream of upload / download (overlaps the transposes)
@@ -173,6 +176,10 @@ struct fsb_engine {
     double* d_cl_bary = nullptr;
     uint64_t cl_cap = 0;
     uint64_t last_launches = 0;
+    int last_strategy = FSB_STRATEGY_AUTO;  // strategy the last run executed
+    std::string fallback;                   // why the last AUTO run left its first choice ("" = it did not)
+    fsb_dev::EatClock* eclk = nullptr;      // eat-region clock (device)
+    double last_eat_s = 0.0;                // eat region of the last run / eat call
 
     std::map<std::pair<uint64_t, int>, GraphEntry> graphs;  // (T, explicit_first | sane << 1)
     ncclComm_t comm = nullptr;
@@ -215,6 +222,53 @@ int exchange(fsb_engine* e, int buf) {
                                       e->stream);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllGather");
     return FSB_OK;
+}
+
+// Eat-region clock links (fsb_kernels.cuh EatClock).
+fsb_dev::EatLink ec_link(const fsb_engine* e, int out_slot, int in_slot, int phase) {
+    fsb_dev::EatLink l{};
+    l.out = out_slot >= 0 ? &e->eclk->s[out_slot] : nullptr;
+    l.in = in_slot >= 0 ? &e->eclk->s[in_slot] : nullptr;
+    l.ns = &e->eclk->ns;
+    l.phase = phase;
+    return l;
+}
+
+int read_eat_ns(fsb_engine* e, double divisor, double* seconds) {
+    unsigned long long ns = 0;
+    CU(cudaMemcpyAsync(&ns, &e->eclk->ns, sizeof ns, cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    *seconds = (double)ns * 1e-9 / (divisor > 0 ? divisor : 1.0);
+    return FSB_OK;
+}
+
+// Persistent kernels: per-CTA SM cycles summed in ns, CTA 0's globaltimer /
+// clock64 brackets convert them; mean over the `ctas` CTAs.
+int read_eat_cycles(fsb_engine* e, double ctas, double* seconds) {
+    fsb_dev::EatClock c{};
+    CU(cudaMemcpyAsync(&c, e->eclk, sizeof c, cudaMemcpyDeviceToHost, e->stream));
+    CU(cudaStreamSynchronize(e->stream));
+    const double ns_per_cycle =
+        (c.c1 > c.c0 && c.g1 > c.g0) ? (double)(c.g1 - c.g0) / (double)(c.c1 - c.c0) : 0.0;
+    *seconds = (double)c.ns * ns_per_cycle * 1e-9 / (ctas > 0 ? ctas : 1.0);
+    return FSB_OK;
+}
+
+// Fault injection for the AUTO fallback tests: FSB_FAULT_INJECT names the
+// launches that should be refused as if the device could not co-schedule them
+// ("grid", "persistent"; comma-separated).  Read at every launch.
+bool fault_injected(const char* what) {
+    const char* v = std::getenv("FSB_FAULT_INJECT");
+    return v && *v && std::strstr(v, what) != nullptr;
+}
+
+// Launch errors that mean "this device cannot co-schedule the persistent
+// grid / cluster right now" (a profiler replay, MPS, a shared or partitioned
+// device): AUTO then runs the graph of step kernels instead.
+bool co_schedule_refused(cudaError_t ce) {
+    return ce == cudaErrorCooperativeLaunchTooLarge || ce == cudaErrorNotSupported ||
+           ce == cudaErrorInvalidClusterSize || ce == cudaErrorLaunchOutOfResources ||
+           ce == cudaErrorNotPermitted;
 }
 
 int guard(fsb_engine* e) {
@@ -290,6 +344,23 @@ bool want_persistent(const fsb_engine* e) {
 // (profiles/r03_ab_grid.jsonl).
 constexpr uint64_t kGridAutoMaxFish = 2500000;
 
+// The shared-memory-resident grid kernel holds the school on chip: every CTA's
+// pair range must fit its shared memory (about 1.06e6 fish on 148 SMs).
+bool fits_sgrid(const fsb_engine* e) {
+    if (!e->sg_cap || (e->flags & (FSB_FLAG_L2_GRID | FSB_FLAG_FLAT_GRID))) return false;
+    const uint64_t npairs = e->count >> 1;
+    const uint64_t per_cta = (npairs + e->sg_grid - 1) / e->sg_grid;
+    return per_cta <= e->sg_cap;
+}
+
+// Nsight Compute (and other CUDA tool injections) cannot replay a cooperative
+// launch of thread-block clusters: it terminates the process instead of
+// returning an error.  With a tool injected, that launch is treated as refused.
+bool tool_injected() {
+    const char* v = std::getenv("CUDA_INJECTION64_PATH");
+    return v && *v;
+}
+
 bool want_grid(const fsb_engine* e) {
     if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode) return false;
     if (e->strategy == FSB_STRATEGY_GRID) return true;
@@ -350,6 +421,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
     int rc = FSB_OK;
     cudaError_t ce = cudaMemcpyAsync(e->d_step0, e->h_step0, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                      e->stream);
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(&e->eclk->ns, 0, sizeof(unsigned long long), e->stream);
     uint64_t launches = 0;
     for (uint64_t k = 0; k < T && ce == cudaSuccess && rc == FSB_OK; ++k) {
         fsb_dev::SoA s = e->s;
@@ -363,6 +435,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         a.part_out = local_part(e, (int)(k & 1));
         a.px = px_of(e, e->d_step0 + 1, k, k + 1);  // consumes epoch base+k, produces base+k+1
         a.pdl = (k > 0 && use_pdl(e)) ? 1 : 0;  // kernel -> kernel edges only
+        a.ec = ec_link(e, (int)(k & 1), k ? (int)((k - 1) & 1) : -1, 0);
         ce = fsb_dev::launch_step(a, (k == 0 && explicit_first) ? e->grid_explicit : e->grid, e->stream);
         ++launches;
         if (ce == cudaSuccess) rc = exchange(e, (int)(k & 1));
@@ -379,6 +452,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         ea.bary_out = g.d_bary + 3 * (T - 1);
         ea.px = px_of(e, e->d_step0 + 1, T, 0);
         ea.pdl = use_pdl(e) ? 1 : 0;
+        ea.ec = ec_link(e, -1, (int)((T - 1) & 1), 0);
         ce = fsb_dev::launch_eat(ea, e->grid_aux, e->stream);
         ++launches;
     }
@@ -417,6 +491,7 @@ int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, do
     if (bary) CU(cudaMemcpyAsync(bary, it->second.d_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     CU(cudaStreamSynchronize(e->stream));
     TRY(elapsed(e, seconds));
+    TRY(read_eat_ns(e, 1.0, &e->last_eat_s));
     e->cur_explicit = false;
     e->max_valid = e->sums_valid = true;
     e->cur_buf = (int)((T - 1) & 1);
@@ -449,7 +524,31 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
     TRY(ensure_run_buffers(e, T));
     fsb_dev::StepArgs base = step_args(e, canonical(e));
     base.part_out = local_part(e, 0);
-    if (e->cgrid_nc > 0) {
+    CU(cudaMemsetAsync(e->eclk, 0, sizeof(fsb_dev::EatClock), e->stream));
+    int ctas = 0;
+    bool sums = true;  // the run leaves the barycentre sums of the last step in part_out
+    cudaError_t ce = cudaSuccess;
+    if (fits_sgrid(e)) {
+        // the school on chip: one CTA per SM holds its pairs in shared memory for all T steps
+        fsb_dev::SGridArgs g{};
+        g.base = base;
+        g.first_step = first_step;
+        g.num_steps = T;
+        g.trace = e->d_cl_trace;
+        g.bary = bary ? e->d_cl_bary : nullptr;
+        g.pair_cap = e->sg_cap;
+        g.eclk = e->eclk;
+        g.gen = e->d_gen;
+        g.parts = e->block_part;  // block_cap >= 2 x grid_coop >= 2 x SMs
+        g.keys = e->d_sg_keys;
+        CU(cudaMemsetAsync(e->d_gen, 0, sizeof(unsigned long long), e->stream));
+        CU(cudaMemsetAsync(e->d_sg_keys, 0, 3 * sizeof(unsigned long long), e->stream));
+        CU(cudaEventRecord(e->ev0, e->stream));
+        ce = fault_injected("grid") ? cudaErrorCooperativeLaunchTooLarge
+                                    : fsb_dev::launch_sgrid_run(g, e->sg_grid, e->stream);
+        ctas = e->sg_grid;
+        sums = bary != nullptr;  // max-only reduction unless the barycentre trace is wanted
+    } else if (e->cgrid_nc > 0) {
         // clusters of 8 CTAs reduce over DSMEM; leaders meet through sentinel slots
         fsb_dev::CGridArgs g{};
         g.base = base;
@@ -458,9 +557,12 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
         g.trace = e->d_cl_trace;
         g.bary = bary ? e->d_cl_bary : nullptr;
         g.cl_slots = e->d_cl_slots;
+        g.eclk = e->eclk;
         CU(cudaMemsetAsync(e->d_cl_slots, 0xFF, cl_slot_bytes(e), e->stream));  // every word the sentinel
         CU(cudaEventRecord(e->ev0, e->stream));
-        CU(fsb_dev::launch_cgrid_run(g, e->cgrid_nc, e->stream));
+        ce = (fault_injected("grid") || tool_injected()) ? cudaErrorNotSupported
+                                                         : fsb_dev::launch_cgrid_run(g, e->cgrid_nc, e->stream);
+        ctas = e->cgrid_nc * fsb_dev::kCGridCluster;
     } else {
         fsb_dev::GridArgs g{};
         g.base = base;
@@ -469,18 +571,29 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
         g.trace = e->d_cl_trace;
         g.bary = bary ? e->d_cl_bary : nullptr;
         g.gen = e->d_gen;
+        g.eclk = e->eclk;
         CU(cudaMemsetAsync(e->d_gen, 0, sizeof(unsigned long long), e->stream));
         CU(cudaEventRecord(e->ev0, e->stream));
-        CU(fsb_dev::launch_grid_run(g, e->grid_coop, e->stream));
+        ce = fault_injected("grid") ? cudaErrorCooperativeLaunchTooLarge
+                                    : fsb_dev::launch_grid_run(g, e->grid_coop, e->stream);
+        ctas = e->grid_coop;
+    }
+    if (ce != cudaSuccess) {
+        cudaGetLastError();  // launch-configuration errors are not sticky
+        const int code = co_schedule_refused(ce) ? FSB_ERR_UNSUPPORTED : FSB_ERR_CUDA;
+        return fail(code, std::string("grid strategy: cooperative launch refused: ") + cudaGetErrorName(ce));
     }
     CU(cudaEventRecord(e->ev1, e->stream));
     if (trace) CU(cudaMemcpyAsync(trace, e->d_cl_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     if (bary) CU(cudaMemcpyAsync(bary, e->d_cl_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     CU(cudaStreamSynchronize(e->stream));
     TRY(elapsed(e, seconds));
-    e->max_valid = e->sums_valid = true;
+    TRY(read_eat_cycles(e, (double)ctas, &e->last_eat_s));
+    e->max_valid = true;
+    e->sums_valid = sums;
     e->cur_buf = 0;
     e->last_launches = 1;
+    e->last_strategy = FSB_STRATEGY_GRID;
     return FSB_OK;
 }
 
@@ -505,21 +618,33 @@ int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace
     a.trace = e->d_cl_trace;
     a.bary = bary ? e->d_cl_bary : nullptr;  // max-only reduction unless sums are wanted
     a.part_out = local_part(e, 0);
+    a.eclk = std::getenv("FSB_NO_EAT_CLOCK") ? nullptr : e->eclk;  // (A/B of the clock's cost)
+    CU(cudaMemsetAsync(e->eclk, 0, sizeof(fsb_dev::EatClock), e->stream));
     CU(cudaEventRecord(e->ev0, e->stream));
-    cudaError_t ce = fsb_dev::launch_cluster_run(a, e->stream);
+    int ctas = 0;
+    cudaError_t ce = fault_injected("persistent") ? cudaErrorInvalidClusterSize
+                                                  : fsb_dev::launch_cluster_run(a, e->stream, &ctas);
     if (ce == cudaErrorNotSupported)
         return fail(FSB_ERR_UNSUPPORTED, "school does not fit the persistent cluster kernel");
-    if (ce != cudaSuccess) return cuda_fail(ce, "cluster kernel launch");
+    if (ce != cudaSuccess) {
+        cudaGetLastError();
+        if (co_schedule_refused(ce))
+            return fail(FSB_ERR_UNSUPPORTED, std::string("persistent strategy: cluster launch refused: ") +
+                                                 cudaGetErrorName(ce));
+        return cuda_fail(ce, "cluster kernel launch");
+    }
     CU(cudaEventRecord(e->ev1, e->stream));
     if (trace) CU(cudaMemcpyAsync(trace, e->d_cl_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     if (bary) CU(cudaMemcpyAsync(bary, e->d_cl_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     CU(cudaStreamSynchronize(e->stream));
     TRY(elapsed(e, seconds));
+    TRY(read_eat_cycles(e, (double)ctas, &e->last_eat_s));
     e->cur_explicit = false;
-    e->max_valid = e->sums_valid = true;
+    e->max_valid = true;
     e->sums_valid = bary != nullptr;
     e->cur_buf = 0;
     e->last_launches = 1;
+    e->last_strategy = FSB_STRATEGY_PERSISTENT;
     return FSB_OK;
 }
 
@@ -534,6 +659,7 @@ int reduce_current(fsb_engine* e) {
     a.part_out = local_part(e, 0);
     a.world = e->world;
     a.px = px_of(e, nullptr, 0, e->xseq + 1);
+    a.ec = ec_link(e, 0, -1, 1);
     // launched even for an empty shard: it publishes the identity partial (and,
     // with a peer exchange, pushes it so the other ranks are not kept waiting)
     CU(fsb_dev::launch_reduce(a, e->grid_aux, e->stream));
@@ -661,10 +787,11 @@ int fsb_engine_destroy(fsb_engine* e) {
     if (e->d_peers) cudaFree(e->d_peers);
     if (e->d_gen) cudaFree(e->d_gen);
     if (e->d_cl_slots) cudaFree(e->d_cl_slots);
+    if (e->d_sg_keys) cudaFree(e->d_sg_keys);
     for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
                     (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
                     (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
-                    (void*)e->d_cl_bary})
+                    (void*)e->d_cl_bary, (void*)e->eclk})
         if (p) cudaFree(p);
     if (e->h_step0) cudaFreeHost(e->h_step0);
     if (e->pinned) cudaFreeHost(e->pinned);
@@ -766,6 +893,14 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     if (e->cgrid_nc > 0) {
         CB(cudaMalloc(&e->d_cl_slots, cl_slot_bytes(e)));
     }
+    if (e->world == 1 && !(e->flags & (FSB_FLAG_L2_GRID | FSB_FLAG_FLAT_GRID))) {
+        e->sg_cap = fsb_dev::sgrid_pair_capacity(e->device, &e->sg_grid);
+        if (e->sg_cap > 0 && 2ull * e->sg_cap * e->sg_grid >= e->count && e->count > 0 &&
+            2 * e->sg_grid <= e->block_cap)
+            CB(cudaMalloc(&e->d_sg_keys, 3 * sizeof(unsigned long long)));
+        else
+            e->sg_cap = 0;
+    }
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
     CB(cudaMalloc(&e->counter, sizeof(unsigned)));
@@ -783,6 +918,8 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
         }
     }
     CB(cudaMalloc(&e->d_scalar, 4 * sizeof(double)));
+    CB(cudaMalloc(&e->eclk, sizeof(fsb_dev::EatClock)));
+    CB(cudaMemset(e->eclk, 0, sizeof(fsb_dev::EatClock)));
     CB(cudaMalloc(&e->d_mismatch, sizeof(int)));
 
     if (e->use_nccl) {
@@ -923,6 +1060,7 @@ int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
         a.part_in = nullptr;  // no pending eat: phases are applied eagerly
         a.part_out = local_part(e, 0);
         a.px = px_of(e, nullptr, 0, e->xseq + 1);
+        a.ec = ec_link(e, 0, -1, 1);  // the fused max: producer side of the eat region
         CU(fsb_dev::launch_step(a, e->cur_explicit ? e->grid_explicit : e->grid, e->stream));
     } else {
         const Partial id{-INFINITY, 0.0, 0.0, 0.0};
@@ -942,7 +1080,7 @@ int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
 int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     TRY(guard(e));
     TRY(need_peers(e));
-    CU(cudaEventRecord(e->ev0, e->stream));
+    CU(cudaMemsetAsync(&e->eclk->ns, 0, sizeof(unsigned long long), e->stream));
     if (!e->max_valid) TRY(reduce_current(e));
     TRY(need_partials(e));
     fsb_dev::EatArgs a{};
@@ -953,12 +1091,14 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     a.world = e->world;
     a.px = px_of(e, nullptr, e->xseq, 0);
     a.trace_out = e->d_scalar;
+    a.ec = ec_link(e, -1, 0, 1);  // consumer side: the producer's reduction tail + this combine
     CU(fsb_dev::launch_eat(a, e->grid_aux, e->stream));
-    CU(cudaEventRecord(e->ev1, e->stream));
     double m = 0.0;
     CU(cudaMemcpyAsync(&m, e->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
-    TRY(elapsed(e, seconds));
     CU(cudaStreamSynchronize(e->stream));
+    // EatResult::seconds (sim.hpp:103): the max only, not the weight update
+    TRY(read_eat_ns(e, 1.0, &e->last_eat_s));
+    if (seconds) *seconds = e->last_eat_s;
     if (max_diff) *max_diff = m;
     return FSB_OK;
 }
@@ -968,7 +1108,7 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
 int run_stream_chunked(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
                        double* seconds) {
     constexpr uint64_t kMaxGraphSteps = 1024;
-    double total = 0.0;
+    double total = 0.0, eat = 0.0;
     uint64_t launches = 0;
     for (uint64_t off = 0; off < T; off += kMaxGraphSteps) {
         const uint64_t len = (T - off < kMaxGraphSteps) ? T - off : kMaxGraphSteps;
@@ -976,10 +1116,13 @@ int run_stream_chunked(fsb_engine* e, uint64_t first_step, uint64_t T, double* t
         TRY(run_stream(e, first_step + off, len, trace ? trace + off : nullptr, bary ? bary + 3 * off : nullptr,
                        &s));
         total += s;
+        eat += e->last_eat_s;
         launches += e->last_launches;
     }
     *seconds = total;
+    e->last_eat_s = eat;
     e->last_launches = launches;
+    e->last_strategy = FSB_STRATEGY_STREAM;
     return FSB_OK;
 }
 
@@ -988,7 +1131,9 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
     TRY(guard(e));
     TRY(need_peers(e));
     TRY(phase_only(e, "fsb_engine_run"));
-    if (timing) *timing = fsb_timing{0.0, 0.0, 0.0};
+    if (timing) *timing = fsb_timing{0.0, 0.0, 0.0, 0.0};
+    e->fallback.clear();
+    e->last_eat_s = 0.0;
     if (num_steps == 0) return FSB_OK;
     double secs = 0.0;
     if (e->count == 0 && !e->use_nccl && !e->peer_mode) {
@@ -1002,21 +1147,31 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
         e->max_valid = e->sums_valid = true;
         e->cur_buf = 0;
         e->last_launches = 0;
+        e->last_strategy = FSB_STRATEGY_STREAM;
     } else if (want_grid(e)) {
         // (the first run after an inconsistent upload takes the stream path below)
-        TRY(run_grid(e, first_step, num_steps, trace, bary, &secs));
+        int rc = run_grid(e, first_step, num_steps, trace, bary, &secs);
+        if (rc == FSB_ERR_UNSUPPORTED && e->strategy == FSB_STRATEGY_AUTO) {
+            e->fallback = g_err;  // the device refused the co-resident grid: graph of step kernels
+            rc = run_stream_chunked(e, first_step, num_steps, trace, bary, &secs);
+        }
+        TRY(rc);
     } else if (want_persistent(e)) {
         int rc = run_persistent(e, first_step, num_steps, trace, bary, &secs);
-        if (rc == FSB_ERR_UNSUPPORTED && e->strategy == FSB_STRATEGY_AUTO)
+        if (rc == FSB_ERR_UNSUPPORTED && e->strategy == FSB_STRATEGY_AUTO) {
+            e->fallback = g_err;
             rc = run_stream_chunked(e, first_step, num_steps, trace, bary, &secs);
+        }
         TRY(rc);
     } else {
         TRY(run_stream_chunked(e, first_step, num_steps, trace, bary, &secs));
     }
     if (timing) {
+        // SimResult (sim.hpp:125-131): seconds_eat = the max region only, seconds_move = the rest of the loop
         timing->seconds_total = secs;
-        timing->seconds_move = secs;
-        timing->seconds_eat = 0.0;
+        timing->seconds_eat = e->last_eat_s < secs ? e->last_eat_s : secs;
+        timing->seconds_move = secs - timing->seconds_eat;
+        timing->seconds_loop = secs;
     }
     return FSB_OK;
 }
@@ -1053,7 +1208,7 @@ int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
     return FSB_OK;
 }
 
-int fsb_engine_partial(fsb_engine* e, double out[4]) {
+int fsb_engine_partial(fsb_engine* e, double out[5]) {
     TRY(guard(e));
     TRY(need_peers(e));
     if (!out) return fail(FSB_ERR_INVALID_ARGUMENT, "null out");
@@ -1065,22 +1220,33 @@ int fsb_engine_partial(fsb_engine* e, double out[4]) {
     out[1] = p.sx;
     out[2] = p.sy;
     out[3] = p.sf;
+    out[4] = (double)e->xseq;  // exchange epoch: identical on every rank at the same step
     return FSB_OK;
 }
 
 int fsb_engine_set_partials(fsb_engine* e, const double* parts, size_t count) {
     TRY(guard(e));
     if (!e->host_xchg) return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials needs FSB_FLAG_HOST_EXCHANGE");
-    if (!parts || count != 4 * (size_t)e->world)
-        return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: need 4 * world_size doubles");
+    if (!parts || count != 5 * (size_t)e->world)
+        return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: need 5 * world_size doubles");
     if (!e->max_valid || !e->sums_valid)
         return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: no partial of the current state (fsb_engine_partial)");
     // this rank's own entry must be its partial, bit for bit: catches partials out of rank order
-    double mine[4];
+    double mine[5];
     TRY(fsb_engine_partial(e, mine));
-    if (std::memcmp(mine, parts + 4 * (size_t)e->rank, sizeof mine) != 0)
+    if (std::memcmp(mine, parts + 5 * (size_t)e->rank, sizeof mine) != 0)
         return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: entry [rank] is not this rank's partial");
-    CU(cudaMemcpyAsync(all_part(e, e->cur_buf), parts, 4 * (size_t)e->world * sizeof(double),
+    // every rank's partial must be of the same step (exchange epoch): catches a
+    // rank that moved twice or skipped a move
+    std::vector<Partial> packed(e->world);
+    for (int q = 0; q < e->world; ++q) {
+        const double* v = parts + 5 * (size_t)q;
+        if (std::memcmp(&v[4], &mine[4], sizeof(double)) != 0)
+            return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials: entry [" + std::to_string(q) +
+                                                      "] is from another step (exchange epoch differs)");
+        packed[q] = Partial{v[0], v[1], v[2], v[3]};
+    }
+    CU(cudaMemcpyAsync(all_part(e, e->cur_buf), packed.data(), (size_t)e->world * sizeof(Partial),
                        cudaMemcpyHostToDevice, e->stream));
     CU(cudaStreamSynchronize(e->stream));
     e->xchg_ready = true;
@@ -1221,6 +1387,13 @@ int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta) {
 int fsb_engine_last_launches(const fsb_engine* e, uint64_t* launches) {
     if (!e || !launches) return fail(FSB_ERR_INVALID_ARGUMENT, "null argument");
     *launches = e->last_launches;
+    return FSB_OK;
+}
+
+int fsb_engine_last_strategy(const fsb_engine* e, int* strategy, const char** fallback_reason) {
+    if (!e || !strategy) return fail(FSB_ERR_INVALID_ARGUMENT, "null argument");
+    *strategy = e->last_strategy;
+    if (fallback_reason) *fallback_reason = e->fallback.c_str();
     return FSB_OK;
 }
 

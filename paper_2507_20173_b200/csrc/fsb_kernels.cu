@@ -79,15 +79,46 @@ __device__ __forceinline__ Partial warp_reduce(Partial v) {
     return v;
 }
 
+// %globaltimer: ns, one clock for every SM (the eat-region clock).
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Persistent kernels: CTA 0 brackets the run with globaltimer and clock64 so
+// the host can convert the per-CTA cycle counts of the eat region into ns.
+__device__ __forceinline__ void eclk_bracket(EatClock* c, bool end) {
+    if (c && blockIdx.x == 0 && threadIdx.x == 0) {
+        const unsigned long long g = gtimer();
+        const unsigned long long k = clock64();
+        if (end) {
+            c->g1 = g;
+            c->c1 = k;
+        } else {
+            c->g0 = g;
+            c->c0 = k;
+        }
+    }
+}
+
+__device__ __forceinline__ void red_max_relaxed_gpu(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Block-wide reduction; the result is valid in warp 0 (all lanes).
+// If stamp != nullptr, thread 0 stores the globaltimer right after the barrier
+// at which every warp of the CTA has finished its fish (the eat-region start).
 // `scratch` holds blockDim/32 partials.  Ends with the caller's warp 0 owning
 // the value; callers __syncthreads() before reusing scratch.
-__device__ __forceinline__ Partial block_reduce(Partial v, Partial* scratch) {
+__device__ __forceinline__ Partial block_reduce(Partial v, Partial* scratch,
+                                                unsigned long long* stamp = nullptr, bool cycles = false) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     v = warp_reduce(v);
     if (lane == 0) scratch[warp] = v;
     __syncthreads();
+    if (stamp && threadIdx.x == 0) *stamp = cycles ? clock64() : gtimer();
     Partial r = identity();
     if (warp == 0) {
         const int nw = blockDim.x >> 5;
@@ -122,12 +153,14 @@ __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long ke
     return (static_cast<unsigned long long>(hi) << 32) | lo;
 }
 // valid in warp 0 (all lanes)
-__device__ __forceinline__ unsigned long long block_max_key(unsigned long long key, unsigned long long* scratch) {
+__device__ __forceinline__ unsigned long long block_max_key(unsigned long long key, unsigned long long* scratch,
+                                                            unsigned long long* stamp = nullptr, bool cycles = false) {
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     key = warp_max_key(key);
     if (lane == 0) scratch[warp] = key;
     __syncthreads();
+    if (stamp && threadIdx.x == 0) *stamp = cycles ? clock64() : gtimer();
     unsigned long long r = kKeyNegInf;
     if (warp == 0) {
         if (lane < (int)(blockDim.x >> 5)) r = scratch[lane];
@@ -230,13 +263,16 @@ __device__ __forceinline__ Partial wait_and_combine_peers(const PeerXchg& px, in
 // index order and publishes this rank's partial (and, with a peer exchange,
 // pushes it to every rank).
 // grid_publish: the CTA total `blk` (valid in thread 0) joins the grid reduction.
+// t_done (thread 0): when this CTA's fish were all updated (eat-region clock).
 __device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs& ws, Partial* part_out,
-                                             const PeerXchg& px, int world) {
+                                             const PeerXchg& px, int world, EatStamp* ec_out,
+                                             unsigned long long t_done) {
     __shared__ Partial scratch[32];
     __shared__ bool am_last;
     if (threadIdx.x == 0) {
         FSB_CHECK(blockIdx.x < ws.cap);
         store_partial(&ws.block_part[blockIdx.x], blk);
+        if (ec_out) red_max_relaxed_gpu(&ec_out->t_done, t_done);  // ordered before the release below
         // release: this CTA's partial before its arrival; acquire: the last
         // arriver sees every partial (the counter's release sequence).  The
         // other threads of the last CTA are ordered after it by the barrier
@@ -252,16 +288,21 @@ __device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs&
     if (threadIdx.x == 0) {
         store_partial(part_out, tot);
         *ws.counter = 0u;  // ready for the next launch
+        if (ec_out) ec_out->t_pub = gtimer();
     }
     const uint64_t epoch = px.peers ? epoch_of(px, px.out_add) : 0ull;
     if (epoch && threadIdx.x < 32) push_to_peers(px, world, epoch, tot);
 }
 
+// t_start != 0: the eat region of this CTA starts there (reduce_kernel: the
+// whole pass is the max); else when its fish are done (block barrier).
 __device__ __forceinline__ void grid_finish(const Partial& local, const ReduceWs& ws, Partial* part_out,
-                                            const PeerXchg& px, int world) {
+                                            const PeerXchg& px, int world, EatStamp* ec_out,
+                                            unsigned long long t_start = 0) {
     __shared__ Partial scratch[32];
-    const Partial blk = block_reduce(local, scratch);
-    grid_publish(blk, ws, part_out, px, world);
+    unsigned long long t_done = t_start;
+    const Partial blk = block_reduce(local, scratch, (ec_out && !t_start) ? &t_done : nullptr);
+    grid_publish(blk, ws, part_out, px, world, ec_out, t_done);
 }
 
 // Programmatic Dependent Launch: block until the predecessor grid has completed
@@ -286,8 +327,19 @@ __device__ __forceinline__ Partial combine_prev(const Partial* part_in, int worl
     return r;
 }
 
-__device__ __forceinline__ void publish_prev(const Partial& prev, double* trace_out, double* bary_out) {
+// Block 0, thread 0 of the kernel that consumes the previous step's max: the
+// trace entries, and the eat-region clock (t_start: this kernel's entry).
+__device__ __forceinline__ void publish_prev(const Partial& prev, double* trace_out, double* bary_out,
+                                             const EatLink& ec, unsigned long long t_start) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (ec.in && ec.ns) {
+            const unsigned long long t_have = gtimer();
+            const EatStamp st = *ec.in;
+            const unsigned long long region =
+                ec.phase ? (st.t_pub - st.t_done) + (t_have - t_start) : t_have - st.t_done;
+            if (st.t_done && st.t_done <= st.t_pub && st.t_done <= t_have) *ec.ns += region;
+            ec.in->t_done = 0ull;  // re-armed for the producer two steps on
+        }
         if (trace_out) *trace_out = prev.best;
         if (bary_out) {
             bary_out[0] = prev.sx;
@@ -560,15 +612,16 @@ __device__ __forceinline__ void step_chunk(const StepArgs& a, const StepParams& 
 template <bool kExplicitCur, bool kSane>
 __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(const StepArgs a) {
     const StepParams P = params_of(a.k);
+    const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
     pdl_wait_and_release();
     const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out);
+    publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
     Partial acc = identity();
     step_chunk<kExplicitCur, kSane>(a, P, eat, M, step, acc);
-    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
+    grid_finish(acc, a.ws, a.part_out, a.px, a.world, a.ec.out);
 }
 
 // ---------------------------------------------------------------------------
@@ -593,9 +646,10 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     // is at the 64-register limit of 1024-thread CTAs
     __shared__ unsigned next_tile, s_ghi, s_gpt, s_ntiles;
     const StepParams P = params_of(a.k);
+    const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
     pdl_wait_and_release();
     const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out);
+    publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
@@ -670,6 +724,7 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
         ++grp;
     }
     __syncthreads();
+    const unsigned long long t_done = (a.ec.out && threadIdx.x == 0) ? gtimer() : 0ull;
     Partial cta = identity();
     if (threadIdx.x < 32) {
         for (unsigned i = lane; i < s_ntiles; i += 32) fold(cta, tile_part[i]);
@@ -687,7 +742,7 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
             fold(cta, tail);
         }
     }
-    grid_publish(cta, a.ws, a.part_out, a.px, a.world);
+    grid_publish(cta, a.ws, a.part_out, a.px, a.world, a.ec.out, t_done);
 }
 
 // ---------------------------------------------------------------------------
@@ -705,13 +760,16 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
     __shared__ Partial scratch[32];
     __shared__ Partial shared_prev;
     Partial prev = identity();  // no pending eat at the start of a run
+    __shared__ unsigned long long t_done, ecl;  // eat-region clock (thread 0; kept out of the step loop's registers)
+    if (threadIdx.x == 0) ecl = 0;
+    eclk_bracket(g.eclk, false);
     for (uint64_t k = 0; k < g.num_steps; ++k) {
         const uint64_t step = g.first_step + k;
         const bool eat = prev.best > 0.0;
         const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
         Partial acc = identity();
         step_chunk<false, kSane>(a, P, eat, M, step, acc);
-        const Partial blk = block_reduce(acc, scratch);
+        const Partial blk = block_reduce(acc, scratch, &t_done, true);
         // Grid exchange: publish the CTA partial into slot [k&1][b], arrive on
         // the monotonic counter, wait for all G arrivals of this step, then
         // EVERY CTA folds the G partials itself in index order (the same tree
@@ -732,6 +790,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
         const Partial tot = block_reduce(t, scratch);
         if (threadIdx.x == 0) {
             shared_prev = tot;
+            ecl += clock64() - t_done;
             if (blockIdx.x == 0) {
                 g.trace[k] = tot.best;
                 if (g.bary) {
@@ -762,6 +821,8 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) grid_kernel(cons
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && g.num_steps) store_partial(a.part_out, prev);
+    if (threadIdx.x == 0 && g.eclk) atomicAdd(&g.eclk->ns, ecl);
+    eclk_bracket(g.eclk, true);
 }
 
 // ---------------------------------------------------------------------------
@@ -834,9 +895,10 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
     __shared__ __align__(8) uint64_t empty[kBulkStages];
 
     const StepParams P = params_of(a.k);
+    const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
     pdl_wait_and_release();
     const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out);
+    publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
@@ -954,15 +1016,16 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
             a.s.p[i] = p;
         }
     }
-    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
+    grid_finish(acc, a.ws, a.part_out, a.px, a.world, a.ec.out);
 }
 
 
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
+    const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
     pdl_wait_and_release();
     const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out);
+    publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
     if (!(prev.best > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
     const SharedDivisor M = make_divisor(prev.best);
     const double half = a.k.half_pond;
@@ -1000,6 +1063,7 @@ __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
 
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceArgs a) {
+    const unsigned long long t_start = a.ec.out ? gtimer() : 0ull;  // the whole pass is the max region
     const double half = a.k.half_pond;
     Partial acc = identity();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1008,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads) reduce_kernel(const ReduceArgs a) {
         const double cur = kExplicitCur ? a.s.c[i] : objective(x, y, half);
         accumulate(acc, x, y, a.s.p[i], cur);
     }
-    grid_finish(acc, a.ws, a.part_out, a.px, a.world);
+    grid_finish(acc, a.ws, a.part_out, a.px, a.world, a.ec.out, t_start | 1ull);
 }
 
 struct FishAoS {
@@ -1108,7 +1172,7 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity
 
 // kBary: also reduce the barycentre sums each step (only when the caller asked
 // for them -- the max alone is a 4x shorter reduction on this latency-bound path).
-template <int F, bool kBary>
+template <int F, bool kBary, bool kClock>
 __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned crank = cluster.block_rank();
@@ -1151,6 +1215,8 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
 
     double M = -INFINITY;
     Partial tot = identity();
+    unsigned long long t_done = 0, ecl = 0;  // eat-region clock (thread 0, SM cycles)
+    if (kClock) eclk_bracket(a.eclk, false);
     double u0[F], u1[F];  // this step's RNG draws, made during the previous barrier
 #pragma unroll
     for (int f = 0; f < F; ++f) draw_units(hf[f], a.first_step, u0[f], u1[f]);
@@ -1178,9 +1244,9 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
             }
         }
         Partial blk = identity();
-        if (kBary) blk = block_reduce(acc, scratch);
+        if (kBary) blk = block_reduce(acc, scratch, kClock ? &t_done : nullptr, true);
         else  // the CTA max travels as its key (bits in .best), decoded after the fold
-            blk.best = __longlong_as_double(static_cast<long long>(block_max_key(max_key(acc.best), scratch_key)));
+            blk.best = __longlong_as_double(static_cast<long long>(block_max_key(max_key(acc.best), scratch_key, kClock ? &t_done : nullptr, true)));
         if (threadIdx.x < 32 && threadIdx.x < ncta) {  // lane r pushes this CTA's partial to CTA r
             const uint32_t dst = cluster_map(smem_u32(&slots[b][crank]), threadIdx.x);
             const uint32_t bar = cluster_map(smem_u32(&xbar[b]), threadIdx.x);
@@ -1195,6 +1261,7 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
 #pragma unroll
         for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
         mbar_wait_cluster(&xbar[b], (unsigned)((k >> 1) & 1));
+        if (kClock && threadIdx.x == 0) ecl += clock64() - t_done;
         tot = identity();
         if (kBary) {  // every warp folds the <= 16 CTA partials itself (fixed butterfly)
             const unsigned lane = threadIdx.x & 31;
@@ -1229,6 +1296,10 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         }
     }
     if (a.num_steps > 0 && crank == 0 && threadIdx.x == 0) store_partial(a.part_out, tot);
+    if (kClock) {
+        if (threadIdx.x == 0) atomicAdd(&a.eclk->ns, ecl);
+        eclk_bracket(a.eclk, true);
+    }
     cluster.sync();  // no CTA retires while a peer could still address its shared memory
 }
 
@@ -1369,6 +1440,9 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(con
     cluster.sync();  // every CTA's barriers exist before anyone pushes into them
 
     double prev_best = -INFINITY;  // no pending eat at the start of a run (only the max is kept live)
+    __shared__ unsigned long long t_done, ecl;  // eat-region clock (thread 0; kept out of the step loop's registers)
+    if (threadIdx.x == 0) ecl = 0;
+    eclk_bracket(g.eclk, false);
     for (uint64_t k = 0; k < g.num_steps; ++k) {
         const unsigned b = (unsigned)(k & 1);
         if (threadIdx.x == 0) {  // may race the incoming pushes: fine
@@ -1380,7 +1454,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(con
         const SharedDivisor M = make_divisor(eat ? prev_best : 1.0);
         Partial acc = identity();
         step_chunk<false, kSane>(a, P, eat, M, step, acc);
-        const Partial blk = block_reduce(acc, scratch);  // every lane of warp 0 holds it
+        const Partial blk = block_reduce(acc, scratch, &t_done, true);  // every lane of warp 0 holds it
         if (threadIdx.x == 0) {  // this CTA's partial into the leader's slot
             const uint32_t dst = cluster_map(smem_u32(&slots[b][sreg_cluster_rank()]), 0);
             const uint32_t bar = cluster_map(smem_u32(&xbar[b]), 0);
@@ -1389,6 +1463,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(con
         }
         if (threadIdx.x < 32 && sreg_cluster_rank() == 0) cgrid_leader_exchange(g, k, slots, tslot, xbar, tbar);
         mbar_wait_cluster(&tbar[b], (unsigned)((k >> 1) & 1));
+        if (threadIdx.x == 0) ecl += clock64() - t_done;
         prev_best = tslot[b].best;
         __syncthreads();  // also a scheduling fence: keeps the step loop's registers in bounds
     }
@@ -1409,7 +1484,191 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(con
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && g.num_steps) store_partial(a.part_out, tslot[(g.num_steps - 1) & 1]);
+    if (threadIdx.x == 0 && g.eclk) atomicAdd(&g.eclk->ns, ecl);
+    eclk_bracket(g.eclk, true);
     cluster.sync();  // no CTA retires while a peer could still address its shared memory
+}
+
+// ---------------------------------------------------------------------------
+// sgrid_kernel: the whole school on chip.  One 1024-thread CTA per SM holds its
+// contiguous range of fish pairs in shared memory (x, y, w, p as double2: 64 B
+// per pair, 216 KB per SM at C0's 1e6 fish) for all T steps of one cooperative
+// launch, so a step touches neither L2 nor HBM; the state is read once at the
+// start and written once at the end (sim.hpp:133-147's loop, init aside).
+// Per step every thread runs its pairs through the fused step, the CTA
+// reduces, and the CTAs meet at a counter barrier (one arrival each, release;
+// thread 0 of every CTA spins with acquire):
+//  * max only (no barycentre trace asked for): the CTA max travels as its
+//    order-preserving 64-bit key (REDUX) through one red.max into a per-step
+//    key slot, so after the barrier every CTA reads ONE word;
+//  * with the barycentre: the CTA partial goes into its slot of step parity
+//    k&1, and after the barrier warp 0 of every CTA folds all G partials in
+//    index order (loads issued up front) -- the same fixed tree everywhere, so
+//    every CTA holds bit-identical totals.
+// No clusters: a plain cooperative launch, which Nsight Compute can replay (it
+// terminates the process on cooperative launches of clusters).
+constexpr unsigned kSGridMaxGrid = 160;  // warp 0 folds <= 5 partials per lane
+
+template <bool kSane, bool kBary>
+__global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs g) {
+    extern __shared__ __align__(16) double2 sg_smem[];
+    const StepArgs& a = g.base;
+    const StepParams P = params_of(a.k);
+    __shared__ Partial scratch[32];
+    __shared__ unsigned long long scratch_key[32];
+    __shared__ Partial shared_tot;
+    __shared__ double tail[4];  // the odd last fish of the school (CTA 0)
+    __shared__ unsigned long long t_done, ecl;  // eat-region clock (thread 0, SM cycles)
+    const unsigned t = threadIdx.x;
+    const uint64_t npairs = a.n >> 1;
+    const uint64_t plo = npairs * blockIdx.x / gridDim.x;
+    const unsigned cnt = (unsigned)(npairs * (blockIdx.x + 1) / gridDim.x - plo);
+    FSB_CHECK(cnt <= g.pair_cap && gridDim.x <= kSGridMaxGrid);
+    double2* sx = sg_smem;
+    double2* sy = sx + g.pair_cap;
+    double2* sw = sy + g.pair_cap;
+    double2* sp = sw + g.pair_cap;
+    const double2* X2 = reinterpret_cast<const double2*>(a.s.x) + plo;
+    const double2* Y2 = reinterpret_cast<const double2*>(a.s.y) + plo;
+    const double2* W2 = reinterpret_cast<const double2*>(a.s.w) + plo;
+    const double2* P2 = reinterpret_cast<const double2*>(a.s.p) + plo;
+    for (unsigned q = t; q < cnt; q += blockDim.x) {
+        sx[q] = X2[q];
+        sy[q] = Y2[q];
+        sw[q] = W2[q];
+        sp[q] = P2[q];
+    }
+    const bool has_tail = (a.n & 1ull) && blockIdx.x == 0;
+    if (has_tail && t == 0) {
+        const uint64_t i = a.n - 1;
+        tail[0] = a.s.x[i];
+        tail[1] = a.s.y[i];
+        tail[2] = a.s.w[i];
+        tail[3] = a.s.p[i];
+    }
+    if (t == 0) ecl = 0;
+    eclk_bracket(g.eclk, false);
+    __syncthreads();
+
+    const SoA2 src{sx, sy, sw, sp, nullptr};
+    double prev_best = -INFINITY;  // no pending eat at the start of a run
+    for (uint64_t k = 0; k < g.num_steps; ++k) {
+        const uint64_t step = g.first_step + k;
+        const bool eat = prev_best > 0.0;
+        const SharedDivisor M = make_divisor(eat ? prev_best : 1.0);
+        Partial acc = identity();
+        for (unsigned q = t; q < cnt; q += blockDim.x) {
+            double2 X[1], Y[1], W[1], Q[1], C[1];
+            const bool valid[1] = {true};
+            const uint64_t qs[1] = {q};
+            const uint64_t gi[1] = {a.gfirst + 2 * (plo + q)};
+            X[0] = sx[q];
+            Y[0] = sy[q];
+            W[0] = sw[q];
+            Q[0] = sp[q];
+            fused_pairs<false, 1, kSane>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
+            sx[q] = X[0];
+            sy[q] = Y[0];
+            sw[q] = W[0];
+            sp[q] = Q[0];
+        }
+        if (has_tail && t == 0) {
+            double x = tail[0], y = tail[1], w = tail[2], p = tail[3];
+            fused_fish(x, y, w, p, objective(x, y, P.half_pond), eat, M, a.gfirst + a.n - 1, step, P, acc);
+            tail[0] = x;
+            tail[1] = y;
+            tail[2] = w;
+            tail[3] = p;
+        }
+        const unsigned long long target = (k + 1) * (unsigned long long)gridDim.x;
+        if (kBary) {
+            const Partial blk = block_reduce(acc, scratch, &t_done, true);  // every lane of warp 0 holds it
+            Partial* slots = g.parts + (k & 1) * gridDim.x;  // reused at k+2: every CTA read it before arriving at k+1
+            if (t == 0) {
+                store_partial(&slots[blockIdx.x], blk);
+                red_add_release_gpu(g.gen, 1ull);
+                while (ld_acquire_gpu(g.gen) < target) {
+                }
+            }
+            __syncthreads();
+            if (t < 32) {
+                Partial v[kSGridMaxGrid / 32];
+#pragma unroll
+                for (unsigned r = 0; r < kSGridMaxGrid / 32; ++r) {
+                    const unsigned i = t + 32 * r;
+                    v[r] = i < gridDim.x ? load_cg(&slots[i]) : identity();
+                }
+                Partial f = identity();
+#pragma unroll
+                for (unsigned r = 0; r < kSGridMaxGrid / 32; ++r) fold(f, v[r]);
+                f = warp_reduce(f);
+                if (t == 0) {
+                    shared_tot = f;
+                    ecl += clock64() - t_done;
+                    if (blockIdx.x == 0) {
+                        g.trace[k] = f.best;
+                        g.bary[3 * k + 0] = f.sx;
+                        g.bary[3 * k + 1] = f.sy;
+                        g.bary[3 * k + 2] = f.sf;
+                    }
+                }
+            }
+        } else {
+            // max only: the key of the CTA max, one red.max per CTA into this step's key slot
+            const unsigned long long key = block_max_key(max_key(acc.best), scratch_key, &t_done, true);
+            if (t == 0) {
+                unsigned long long* slot = g.keys + k % 3;
+                red_max_relaxed_gpu(slot, key);
+                red_add_release_gpu(g.gen, 1ull);  // orders the red.max before the arrival
+                while (ld_acquire_gpu(g.gen) < target) {
+                }
+                const double m = key_value(*reinterpret_cast<volatile unsigned long long*>(slot));
+                // slot (k+2)%3 was last read at step k-1 by every CTA (all arrived at k since):
+                // clear it for step k+2; this CTA's arrival at k+1 (release) publishes the clear
+                if (blockIdx.x == 0) g.keys[(k + 2) % 3] = 0ull;
+                shared_tot.best = m;
+                ecl += clock64() - t_done;
+                if (blockIdx.x == 0) g.trace[k] = m;
+            }
+        }
+        __syncthreads();
+        prev_best = shared_tot.best;
+    }
+    // trailing eat of the last step, then the state goes back to HBM
+    const bool eat = prev_best > 0.0 && g.num_steps;
+    const SharedDivisor M = make_divisor(eat ? prev_best : 1.0);
+    double2* Xo = reinterpret_cast<double2*>(a.s.x) + plo;
+    double2* Yo = reinterpret_cast<double2*>(a.s.y) + plo;
+    double2* Wo = reinterpret_cast<double2*>(a.s.w) + plo;
+    double2* Po = reinterpret_cast<double2*>(a.s.p) + plo;
+    for (unsigned q = t; q < cnt; q += blockDim.x) {
+        const double2 x = sx[q], y = sy[q], p = sp[q];
+        double2 w = sw[q];
+        if (eat) {
+            w.x = eat_weight(w.x, p.x, objective(x.x, y.x, P.half_pond), M, P.w_max);
+            w.y = eat_weight(w.y, p.y, objective(x.y, y.y, P.half_pond), M, P.w_max);
+        }
+        Xo[q] = x;
+        Yo[q] = y;
+        Wo[q] = w;
+        Po[q] = p;
+    }
+    if (has_tail && t == 0) {
+        const uint64_t i = a.n - 1;
+        double w = tail[2];
+        if (eat) w = eat_weight(w, tail[3], objective(tail[0], tail[1], P.half_pond), M, P.w_max);
+        a.s.x[i] = tail[0];
+        a.s.y[i] = tail[1];
+        a.s.w[i] = w;
+        a.s.p[i] = tail[3];
+    }
+    if (blockIdx.x == 0 && t == 0 && g.num_steps) {
+        Partial last = shared_tot;
+        if (!kBary) last.sx = last.sy = last.sf = 0.0;  // max only: sums not kept (engine marks them invalid)
+        store_partial(a.part_out, last);
+    }
+    if (t == 0 && g.eclk) atomicAdd(&g.eclk->ns, ecl);
+    eclk_bracket(g.eclk, true);
 }
 
 int g_num_sms[64] = {0};
@@ -1538,6 +1797,60 @@ cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st) {
                                        0, st);
 }
 
+
+#define FSB_SGRID_KERNELS(X) X(false, false) X(false, true) X(true, false) X(true, true)
+
+unsigned sgrid_pair_capacity(int device, int* grid) {
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (num_sms(device) > (int)kSGridMaxGrid) return 0;
+    size_t stat = 0;
+    bool ok = true;
+#define FSB_SG_STAT(S, B)                                                   \
+    {                                                                       \
+        cudaFuncAttributes fa{};                                            \
+        ok = ok && cudaFuncGetAttributes(&fa, sgrid_kernel<S, B>) == cudaSuccess; \
+        if (fa.sharedSizeBytes > stat) stat = fa.sharedSizeBytes;           \
+    }
+    FSB_SGRID_KERNELS(FSB_SG_STAT)
+#undef FSB_SG_STAT
+    if (!ok || (size_t)optin <= stat + 1024) {
+        cudaGetLastError();
+        return 0;
+    }
+    const size_t dyn = ((size_t)optin - stat) / 64 * 64;
+#define FSB_SG_SET(S, B)                                                                                 \
+    {                                                                                                    \
+        int per_sm = 0;                                                                                  \
+        ok = ok && cudaFuncSetAttribute(sgrid_kernel<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        (int)dyn) == cudaSuccess;                                        \
+        ok = ok && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sgrid_kernel<S, B>,            \
+                                                                 kSGridThreads, dyn) == cudaSuccess &&   \
+             per_sm >= 1;                                                                                \
+    }
+    FSB_SGRID_KERNELS(FSB_SG_SET)
+#undef FSB_SG_SET
+    if (!ok) {
+        cudaGetLastError();
+        return 0;
+    }
+    if (grid) *grid = num_sms(device);
+    return (unsigned)(dyn / 64);
+}
+
+cudaError_t launch_sgrid_run(const SGridArgs& g, int grid, cudaStream_t st) {
+    void* args[] = {const_cast<SGridArgs*>(&g)};
+    const bool sane = g.base.sane != 0, bary = g.bary != nullptr;
+    const void* kern = sane ? (bary ? reinterpret_cast<const void*>(sgrid_kernel<true, true>)
+                                    : reinterpret_cast<const void*>(sgrid_kernel<true, false>))
+                            : (bary ? reinterpret_cast<const void*>(sgrid_kernel<false, true>)
+                                    : reinterpret_cast<const void*>(sgrid_kernel<false, false>));
+    return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kSGridThreads), args, (size_t)g.pair_cap * 64, st);
+}
+
 namespace {
 cudaLaunchConfig_t cgrid_config(int clusters, cudaStream_t st, cudaLaunchAttribute (&at)[2]) {
     cudaLaunchConfig_t cfg = {};
@@ -1622,10 +1935,9 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
     (void)device;
     static int cached = 0;
     if (!cached) {
-        cudaFuncSetAttribute(cluster_kernel<1, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(cluster_kernel<1, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(cluster_kernel<kClusterF, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        cudaFuncSetAttribute(cluster_kernel<kClusterF, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        for (auto k : {cluster_kernel<kClusterF, true, true>, cluster_kernel<kClusterF, false, true>,
+                       cluster_kernel<kClusterF, true, false>, cluster_kernel<kClusterF, false, false>})
+            cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cached = 8;
         for (int c : {16, 8}) {
             cudaLaunchConfig_t cfg = {};
@@ -1639,7 +1951,7 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<1, true>, &cfg) == cudaSuccess &&
+            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<kClusterF, true, true>, &cfg) == cudaSuccess &&
                 nclusters >= 1) {
                 cached = c;
                 break;
@@ -1652,7 +1964,7 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
     return cached * 1024;  // one fish per thread, at most 1024 threads per CTA
 }
 
-cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
+cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st, int* ctas) {
     int dev = 0;
     cudaGetDevice(&dev);
     int cmax = 8;
@@ -1679,8 +1991,13 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true>, a);
-    return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false>, a);
+    if (ctas) *ctas = (int)ncta;
+    if (a.eclk) {
+        if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true, true>, a);
+        return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false, true>, a);
+    }
+    if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true, false>, a);
+    return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false, false>, a);
 }
 
 }  // namespace fsb_dev

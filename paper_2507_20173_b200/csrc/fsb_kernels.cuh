@@ -153,6 +153,40 @@ struct PeerXchg {
     uint64_t out_add;          // ... + out_add: epoch of the partial produced (0 = none)
 };
 
+// Eat-region clock: the GPU counterpart of SimResult::seconds_eat, which the
+// reference times around the max only (sim.hpp:103,112,130).  On the GPU the
+// max is fused into the step kernels, so its cost is measured where it sits on
+// the critical path, with %globaltimer (ns, one clock for every SM):
+//  * stream path: from the moment the last CTA of step t has updated its fish
+//    (t_done, max over CTAs by red.max) to the moment step t+1's kernel (or the
+//    trailing eat kernel) holds the combined global max -- the block and grid
+//    reductions, the kernel boundary that is the grid-wide barrier, and any
+//    NCCL / peer exchange in between;
+//  * phase API (move, then eat as separate calls): the producer's reduction
+//    tail (t_done -> t_pub, rank partial published) plus the eat kernel's own
+//    combine, without the host gap between the two calls;
+//  * persistent kernels: every CTA's time from its own fish done to holding the
+//    step's global max, summed, divided by the CTA count by the host.
+struct EatStamp {
+    unsigned long long t_done;  // max over CTAs: all fish of the step updated
+    unsigned long long t_pub;   // the step's rank partial published (last CTA)
+};
+struct EatClock {
+    EatStamp s[2];              // by step parity (graph) / slot 0 (eager launches)
+    unsigned long long ns;      // accumulated eat-region nanoseconds (persistent kernels: SM cycles)
+    unsigned long long pad;
+    // persistent kernels count SM cycles (clock64: a globaltimer read per step
+    // costs ~0.1 us on the 0.9 us C4 step); CTA 0 brackets the kernel with both
+    // clocks so the host converts cycles to ns
+    unsigned long long g0, c0, g1, c1;
+};
+struct EatLink {
+    EatStamp* out;              // producer: this step's stamp (nullptr: off)
+    EatStamp* in;               // consumer: the stamp of the step whose max is combined (nullptr: none)
+    unsigned long long* ns;     // accumulator (nullptr: off)
+    int phase;                  // consumer mode: 1 = phase API (tail + own combine), 0 = graph chain
+};
+
 struct StepArgs {
     SoA s;
     Scalars k;
@@ -172,6 +206,7 @@ struct StepArgs {
     PeerXchg px;          // peer exchange instead of part_in/part_out (px.peers != nullptr)
     int sane;             // state and config in range: guards elided (fsb_math.cuh "In-range mode")
     int dyn;              // compact LDG path: step_kernel_dyn (one CTA per SM, claimed tiles)
+    EatLink ec;           // eat-region clock
 };
 
 // Persistent cooperative-grid run (FSB_STRATEGY_GRID): `base` supplies the
@@ -183,6 +218,7 @@ struct GridArgs {
     double* trace;              // [num_steps]
     double* bary;               // [3*num_steps] or nullptr
     unsigned long long* gen;    // arrival counter, zero at launch; base.ws.block_part holds 2 x grid slots
+    EatClock* eclk;             // eat-region clock (nullptr: off)
 };
 
 // Cluster-reduced persistent run (FSB_STRATEGY_GRID when cluster launch is
@@ -203,6 +239,26 @@ struct CGridArgs {
     double* trace;                // [num_steps]
     double* bary;                 // [3*num_steps] or nullptr
     double* cl_slots;             // [kSlotRing][clusters][kSlotWords], all bytes 0xFF (sentinel) at launch
+    EatClock* eclk;               // eat-region clock (nullptr: off)
+};
+
+// Shared-memory-resident persistent run (FSB_STRATEGY_GRID for schools that
+// fit on chip, ~1.06e6 fish on 148 SMs): one 1024-thread CTA per SM, the CTA's
+// contiguous range of fish pairs held in shared memory for all num_steps steps,
+// one cooperative launch (no clusters: Nsight Compute can replay it); the CTAs
+// meet at a counter barrier each step.
+constexpr int kSGridThreads = 1024;
+struct SGridArgs {
+    StepArgs base;                // state (read at launch, written back at the end), scalars, n, gfirst
+    uint64_t first_step;
+    uint64_t num_steps;
+    double* trace;                // [num_steps]
+    double* bary;                 // [3*num_steps] or nullptr
+    unsigned pair_cap;            // pairs of shared-memory state per CTA (dynamic smem = 64 B each)
+    EatClock* eclk;               // eat-region clock (nullptr: off)
+    unsigned long long* gen;      // arrival counter, zero at launch
+    Partial* parts;               // [2][grid] CTA partials (barycentre runs)
+    unsigned long long* keys;     // [3] per-step max keys (max-only runs), zero at launch
 };
 
 struct EatArgs {
@@ -215,6 +271,7 @@ struct EatArgs {
     double* bary_out;
     int pdl;
     PeerXchg px;
+    EatLink ec;
 };
 
 struct ReduceArgs {
@@ -225,6 +282,7 @@ struct ReduceArgs {
     Partial* part_out;
     PeerXchg px;
     int world;
+    EatLink ec;           // producer only; t_done = kernel start (the whole pass is the max region)
 };
 
 struct InitArgs {
@@ -246,6 +304,7 @@ struct ClusterArgs {
     double* trace;        // [num_steps]
     double* bary;         // [3*num_steps] or nullptr
     Partial* part_out;    // final step partial (for a later eat())
+    EatClock* eclk;       // eat-region clock: per-CTA cycles summed in ns, brackets in g/c (nullptr: off)
 };
 
 int step_grid_blocks(int device, bool explicit_cur, bool bulk);
@@ -267,10 +326,15 @@ int grid_kernel_blocks(int device);
 int cgrid_clusters(int device);
 cudaError_t launch_cgrid_run(const CGridArgs& g, int clusters, cudaStream_t st);
 cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st);
+// Shared-memory-resident grid: the largest number of fish pairs one CTA can
+// hold (0: not available) for a grid of `grid` CTAs (one per SM).
+unsigned sgrid_pair_capacity(int device, int* grid);
+cudaError_t launch_sgrid_run(const SGridArgs& g, int grid, cudaStream_t st);
 
 // Cluster kernel: returns cudaErrorNotSupported when n does not fit.
 int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta);
-cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st);
+// *ctas (may be null) receives the CTA count launched.
+cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st, int* ctas = nullptr);
 
 // Self-test of the guarded fast fp64 paths vs __ddiv_rn / __dsqrt_rn on n
 // generated operands; out[4] (device) accumulates the counts (see .cu).

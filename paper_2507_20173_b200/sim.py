@@ -136,7 +136,8 @@ class Engine:
                  nccl_unique_id: Optional[bytes] = None, strategy: str = "auto",
                  alternate: bool = True, force_nccl: bool = False, bulk=False, pdl: bool = True,
                  peer: bool = False, checked: bool = False, static_tiles: bool = False,
-                 dynamic_tiles: bool = False, flat_grid: bool = False, host_exchange: bool = False):
+                 dynamic_tiles: bool = False, flat_grid: bool = False, host_exchange: bool = False,
+                 l2_grid: bool = False):
         self.cfg = cfg
         L = N.lib()
         self._uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
@@ -145,7 +146,7 @@ class Engine:
                  | (0 if pdl else N.FLAG_NO_PDL) | (N.FLAG_PEER_EXCHANGE if peer else 0)
                  | (N.FLAG_CHECKED if checked else 0) | (N.FLAG_STATIC_TILES if static_tiles else 0)
                  | (N.FLAG_DYNAMIC_TILES if dynamic_tiles else 0) | (N.FLAG_FLAT_GRID if flat_grid else 0)
-                 | (N.FLAG_HOST_EXCHANGE if host_exchange else 0))
+                 | (N.FLAG_HOST_EXCHANGE if host_exchange else 0) | (N.FLAG_L2_GRID if l2_grid else 0))
         opts = N.fsb_engine_options(device, rank, world_size,
                                     ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,
                                     STRATEGIES[strategy], flags)
@@ -226,13 +227,14 @@ class Engine:
         return sums, xy
 
     def partial(self) -> np.ndarray:
-        """This rank's partial of the current state: [max(prev-cur), sum x*f, sum y*f, sum f]."""
-        out = np.empty(4, dtype=np.float64)
+        """This rank's partial of the current state: [max(prev-cur), sum x*f, sum y*f, sum f, epoch]
+        (epoch = the exchange sequence number, equal on every rank at the same step)."""
+        out = np.empty(5, dtype=np.float64)
         N.check(N.lib().fsb_engine_partial(self._h, _ptr(out)))
         return out
 
     def set_partials(self, parts) -> None:
-        """Host exchange engines: every rank's partial() in rank order (world_size x 4)."""
+        """Host exchange engines: every rank's partial() in rank order (world_size x 5)."""
         a = np.ascontiguousarray(parts, dtype=np.float64).reshape(-1)
         N.check(N.lib().fsb_engine_set_partials(self._h, _ptr(a), a.shape[0]))
 
@@ -286,6 +288,13 @@ class Engine:
         v = ctypes.c_uint64()
         N.check(N.lib().fsb_engine_last_launches(self._h, ctypes.byref(v)))
         return v.value
+
+    def last_strategy(self):
+        """(strategy the last run executed: "stream" | "persistent" | "grid", fallback reason or "")."""
+        v, why = ctypes.c_int(), ctypes.c_char_p()
+        N.check(N.lib().fsb_engine_last_strategy(self._h, ctypes.byref(v), ctypes.byref(why)))
+        name = {v_: k for k, v_ in STRATEGIES.items()}.get(v.value, str(v.value))
+        return name, (why.value or b"").decode(errors="replace")
 
 
 class GpuExecutor:

@@ -58,7 +58,7 @@ def test_flag_constants_match_header():
 
 
 def test_abi_version():
-    assert fsb.lib().fsb_abi_version() == 1
+    assert fsb.lib().fsb_abi_version() == N.ABI_VERSION == 2
 
 
 def test_config_validation_matches_reference():

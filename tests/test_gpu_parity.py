@@ -639,3 +639,87 @@ def test_c3_billion_fish(golden_baseline, orc):
         if g:
             assert f"{eng.checksum():016x}" == g["final_checksum"]
             assert rel_ok(bary[-1], [unhex(v) for v in g["barycentre_fsum"]])
+
+
+# ---- AUTO fallback when the device refuses the co-resident launch -----------------
+@pytest.mark.parametrize("n,what", [(100_003, "grid"), (4096, "persistent")])
+def test_auto_falls_back_when_launch_refused(orc, monkeypatch, n, what):
+    """A profiler replay, MPS or a shared device can refuse the cooperative /
+    cluster launch; AUTO then runs the graph of step kernels (bit-exact), an
+    explicit request fails loudly (FSB_FAULT_INJECT refuses the launch)."""
+    cfg = fsb.baseline_config(n, 6)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg) as eng:
+        eng.simulate(barycentre=False)
+        assert eng.last_strategy() == (what, "")
+    monkeypatch.setenv("FSB_FAULT_INJECT", what)
+    with make(cfg) as eng:
+        trace, _, t = eng.simulate(barycentre=False)
+        strat, why = eng.last_strategy()
+        got = eng.download()
+    assert strat == "stream" and "refused" in why, (strat, why)
+    assert trace.tobytes() == want_trace.tobytes()
+    assert got.tobytes() == want_fish.tobytes()
+    with make(cfg, what) as eng:
+        with pytest.raises(fsb.FsbError, match="refused"):
+            eng.simulate(barycentre=False)
+
+
+# ---- eat-region time (SimResult::seconds_eat, sim.hpp:103,112,130) -------------------
+@pytest.mark.parametrize("strategy,n", [("stream", 200_003), ("stream", 3_000_001), ("grid", 200_003),
+                                        ("persistent", 4096)])
+def test_seconds_eat_is_measured(strategy, n):
+    """The max region is measured on the device: positive, below the loop time,
+    and the two add up to the loop (the reference's validate_records rules,
+    csv.hpp:161-179)."""
+    cfg = fsb.baseline_config(n, 20)
+    with make(cfg, strategy) as eng:
+        eng.init()
+        eng.run(0, 5)
+        _, _, t = eng.run(5, 20)
+        assert eng.last_strategy()[0] == strategy
+    assert 0.0 < t.seconds_eat < t.seconds_loop
+    assert t.seconds_move == pytest.approx(t.seconds_loop - t.seconds_eat, rel=1e-12)
+    # a step's max costs at least a CTA reduction and at most the step
+    per = t.seconds_eat / 20
+    assert 2e-7 < per < t.seconds_loop / 20, per
+
+
+def test_flat_grid_seconds_eat():
+    cfg = fsb.baseline_config(100_003, 10)
+    with make(cfg, "grid", flat_grid=True) as eng:
+        _, _, t = eng.simulate(barycentre=False)
+    assert 0.0 < t.seconds_eat < t.seconds_loop
+
+
+def test_phase_eat_seconds_is_the_max_only(orc):
+    cfg = fsb.baseline_config(500_001, 3)
+    with make(cfg) as eng:
+        eng.init()
+        eng.move(0)
+        r = eng.eat()
+        assert 0.0 < r.seconds < 1e-3
+        # after an upload the max needs its own pass over the school: still only the max
+        eng.upload(eng.download())
+        r2 = eng.eat()
+        assert 0.0 < r2.seconds < 1e-3
+
+
+# ---- the shared-memory-resident grid (school on chip for all steps) ---------------
+@pytest.mark.parametrize("n,t", [(16_385, 7), (300_001, 5), (1_000_000, 4), (1_050_001, 3), (1_100_001, 3)])
+def test_smem_grid_and_l2_grid_bit_exact(orc, n, t):
+    """Up to ~1.06e6 fish the grid strategy keeps every CTA's pairs in shared
+    memory; past that (and with l2_grid) the L2-resident cluster grid runs.
+    Both are bit-exact with the oracle; the sums within 1e-12."""
+    cfg = fsb.baseline_config(n, t)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    ref = orc.barycentre_sums(want_fish)
+    for l2 in (False, True):
+        with make(cfg, "grid", l2_grid=l2) as eng:
+            trace, bary, tm = eng.simulate(barycentre=True)
+            got = eng.download()
+            assert eng.last_strategy()[0] == "grid"
+        assert trace.tobytes() == want_trace.tobytes(), (n, l2)
+        assert got.tobytes() == want_fish.tobytes(), (n, l2)
+        assert rel_ok(bary[-1], ref), (n, l2)
+        assert 0.0 < tm.seconds_eat < tm.seconds_loop

@@ -87,6 +87,31 @@ def test_sharded_phases_match_unsharded_oracle(orc, n, steps, world, kw):
             e.close()
 
 
+def test_host_exchange_rejects_partials_of_another_step(orc):
+    """A rank that moved twice (or skipped a move) carries another exchange
+    epoch in its partial: set_partials refuses the gathered set on every rank."""
+    cfg = fsb.baseline_config(10_000, 3)
+    engs = _shards(cfg, 2)
+    try:
+        for e in engs:
+            e.init()
+            e.move(0)
+        engs[0].move(1)
+        parts = np.stack([e.partial() for e in engs])
+        assert parts.shape == (2, 5) and parts[0, 4] != parts[1, 4]
+        for e in engs:
+            with pytest.raises(fsb.FsbError, match="another step"):
+                e.set_partials(parts)
+        engs[1].move(1)
+        parts = np.stack([e.partial() for e in engs])
+        for e in engs:
+            e.set_partials(parts)
+        assert bits(engs[0].eat().max_diff) == bits(engs[1].eat().max_diff)
+    finally:
+        for e in engs:
+            e.close()
+
+
 def test_host_exchange_errors(orc):
     cfg = fsb.baseline_config(10_000, 3)
     engs = _shards(cfg, 2)
@@ -150,7 +175,7 @@ def _gloo_worker(rank, world, port, n, steps, ret):
         for t in range(steps):
             e.move(t)
             mine = torch.from_numpy(e.partial())
-            got = [torch.empty(4, dtype=torch.float64) for _ in range(world)]
+            got = [torch.empty(5, dtype=torch.float64) for _ in range(world)]
             dist.all_gather(got, mine)
             e.set_partials(torch.stack(got).numpy())
             trace.append(e.eat().max_diff)

@@ -35,7 +35,7 @@ for n, t in sizes:
         for k, e in engs.items():
             e.init()
             _, _, tm = e.run(0, t)
-            times[k].append(tm.seconds_move / t * 1e6)
+            times[k].append(tm.seconds_loop / t * 1e6)
     for e in engs.values():
         e.close()
     print(json.dumps({"fish": n, **{k: [round(statistics.median(v), 2), round(min(v), 2), round(max(v), 2)]

@@ -44,7 +44,7 @@ def time_cfg(name, n, t, strategy, alternate, reps, bulk=False, pdl=True, checke
         for r in range(reps):
             eng.init()
             _, _, tm = eng.run(0, t)
-            secs.append(tm.seconds_move)
+            secs.append(tm.seconds_loop)
         s = statistics.median(secs)
         ck = None
     rate = n * t / s

@@ -25,6 +25,6 @@ for n in (2_000, 100_000, 1_000_000, 10_000_000):
             for _ in range(5):
                 eng.init()
                 _, _, t = eng.run(0, T)
-                us.append(t.seconds_move / T * 1e6)
+                us.append(t.seconds_loop / T * 1e6)
             print(json.dumps({"strategy": STRATEGY, "fish": n, "ctas": ctas,
                               "us_per_step": round(statistics.median(us), 3)}), flush=True)
