@@ -1,18 +1,30 @@
 """Command line: the reference's `fsb simulate` / `fsb exp*` on the B200 engine.
 
     python -m paper_2507_20173_b200 simulate [--fish N] [--steps T] [--seed S]
-                                             [--strategy auto|stream|persistent]
+                                             [--strategy auto|stream|persistent|grid]
                                              [--device D] [--out PATH]
-    python -m paper_2507_20173_b200 gpuexp   [--fish N] [--steps T] [--seed S]
+    python -m paper_2507_20173_b200 gpuexp   [--exp 1|3|all] [--fish N] [--steps T] [--seed S]
                                              [--reps R] [--warmup W] [--out PATH]
+    torchrun --nproc-per-node G -m paper_2507_20173_b200 gpuexp --exp 3 ...   (the G axis)
 
 `simulate` mirrors cli.hpp:179-207: one record in the reference CSV schema
 (records.py) to stdout or --out, and the human-readable line
 "total <s> s, eat <s> s, checksum <hex>" to stderr (stdout when --out is given).
-`gpuexp` is the GPU analogue of the paper's configuration sweeps (bench.hpp:
-79-148): the step-loop strategies and step kernels of this
-engine, `reps` measured repetitions after `warmup` discarded ones, one record
-each.  SimConfig keeps the reference CLI's defaults (only fish/steps/seed are
+
+`gpuexp` is the GPU analogue of the paper's sweeps (bench.hpp:79-148;
+PAPER.md:118-131), `reps` measured repetitions after `warmup` discarded ones,
+one record each:
+  * Exp 1 (thread scaling, bench.hpp:79-103): the step kernel's grid from an
+    eighth of the SMs to 8 CTAs per SM -- the fish-per-thread axis (`chunk`);
+  * Exp 3 (aggregation constructs, bench.hpp:132-148): the GPU's ways of
+    computing the step's global max -- last-CTA fold across a kernel
+    boundary, in-graph NCCL allgather, NVLink peer window, cluster DSMEM +
+    leader slots, shared-memory grid counter barrier, flat counter barrier,
+    REDUX + DSMEM in one cluster -- each with its eat-region time
+    (SimResult::seconds_eat, measured on the device), times the GPU count G
+    (one rank per GPU under torchrun; the multi-rank constructs are the NCCL
+    and peer exchanges).
+SimConfig keeps the reference CLI's defaults (only fish/steps/seed are
 settable, cli.hpp:66-79).  Exit codes follow cli.hpp:251-255: 0 ok, 1 runtime
 failure, 2 usage error.
 """
@@ -20,6 +32,7 @@ from __future__ import annotations
 
 import argparse
 import math
+import os
 import sys
 
 from . import records, sim
@@ -38,13 +51,28 @@ def _sms(device: int) -> int:
         return 148
 
 
-def _record(experiment, strategy, cfg, eng, t, rep, threads=1) -> records.BenchRecord:
-    # threads = GPU threads of the step kernel's grid; chunk = fish per thread
-    return records.BenchRecord(experiment=experiment, threads=threads,
-                               schedule="cluster" if strategy == "persistent" else "graph",
-                               chunk=max(1, cfg.num_fish // threads), construct="gpu", rep=rep, fish=cfg.num_fish,
-                               steps=cfg.num_steps, seconds_total=t.seconds_total, seconds_eat=t.seconds_eat,
-                               checksum=eng.checksum())
+SCHEDULE = {"stream": "graph", "persistent": "cluster", "grid": "grid"}
+
+
+def _record(experiment, eng, cfg, t, rep, construct="gpu", gpus=1, gpu_threads=None,
+            checksum=None) -> records.BenchRecord:
+    """threads = GPUs (the team running the construct), schedule = the step
+    loop the engine executed, chunk = fish per GPU thread (records.py)."""
+    used, _ = eng.last_strategy()
+    if gpu_threads is None:
+        ctas, tpc = eng.grid()
+        gpu_threads = ctas * tpc
+    return records.BenchRecord(experiment=experiment, threads=gpus, schedule=SCHEDULE.get(used, used),
+                               chunk=max(1, cfg.num_fish // max(1, gpus * gpu_threads)), construct=construct,
+                               rep=rep, fish=cfg.num_fish, steps=cfg.num_steps, seconds_total=t.seconds_total,
+                               seconds_eat=t.seconds_eat,
+                               checksum=eng.checksum() if checksum is None else checksum)
+
+
+def _failed(experiment, construct, cfg, gpus, schedule="graph") -> records.BenchRecord:
+    # bench.hpp:182-188: a failed cell becomes one NaN row
+    return records.BenchRecord(experiment, gpus, schedule, 0, construct, 0, cfg.num_fish, cfg.num_steps,
+                               math.nan, math.nan, 0)
 
 
 def _emit(recs, out_path, err) -> int:
@@ -63,11 +91,9 @@ def _emit(recs, out_path, err) -> int:
 def cmd_simulate(a) -> int:
     cfg = _config(a)
     cfg.validate()
-    strategy = a.strategy
-    with sim.Engine(cfg, device=a.device, strategy=strategy) as eng:
+    with sim.Engine(cfg, device=a.device, strategy=a.strategy) as eng:
         _, _, t = eng.simulate(barycentre=False)
-        used = "persistent" if eng.last_launches() == 1 and cfg.num_steps > 0 else "stream"
-        rec = _record("custom", used, cfg, eng, t, 0)
+        rec = _record("custom", eng, cfg, t, 0)
     rc = _emit([rec], a.out, sys.stderr)
     if rc:
         return rc
@@ -77,31 +103,113 @@ def cmd_simulate(a) -> int:
     return 0
 
 
+# ---- Exp 1 analogue: grid size / fish per thread ------------------------------------
+def exp1(a, cfg) -> list:
+    sms = _sms(a.device)
+    recs = []
+    for ctas in sorted({max(1, sms // 8), max(1, sms // 4), max(1, sms // 2), sms, 2 * sms, 4 * sms, 8 * sms}):
+        try:
+            with sim.Engine(cfg, device=a.device, strategy="stream", static_tiles=True) as eng:
+                eng.set_grid(ctas)
+                for r in range(a.warmup + a.reps):
+                    _, _, t = eng.simulate(barycentre=False)
+                    if r >= a.warmup:
+                        recs.append(_record("gpu-exp1", eng, cfg, t, r - a.warmup, construct="gpu-lastcta"))
+        except Exception as e:
+            sys.stderr.write(f"gpu-exp1 ctas={ctas}: {e}\n")
+            recs.append(_failed("gpu-exp1", "gpu-lastcta", cfg, 1))
+    return recs
+
+
+# ---- Exp 3 analogue: reduction constructs x G ---------------------------------------
+# (construct, engine kwargs, multi-rank capable)
+CONSTRUCTS = [
+    ("gpu-lastcta", dict(strategy="stream"), False),
+    ("gpu-nccl", dict(strategy="stream", force_nccl=True), True),
+    ("gpu-peer", dict(strategy="stream", peer=True), True),
+    ("gpu-smem-counter", dict(strategy="grid"), False),
+    ("gpu-cluster-slots", dict(strategy="grid", l2_grid=True), False),
+    ("gpu-flat-counter", dict(strategy="grid", flat_grid=True), False),
+    ("gpu-redux-dsmem", dict(strategy="persistent"), False),
+]
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world == 1:
+        return 1, 0, None
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        dist.init_process_group("gloo")  # host-side plumbing only (uids, handles, times); the data path is NCCL/NVLink
+    return world, dist.get_rank(), dist
+
+
+def _chained_checksum(eng, world, rank, dist) -> int:
+    """fsb::checksum (sim.hpp:158-176) over the whole school: FNV-1a continued
+    shard by shard in rank order."""
+    h = sim.kChecksumEmpty
+    for r in range(world):
+        if rank == r:
+            h = eng.checksum(h)
+        if dist is not None:
+            obj = [h]
+            dist.broadcast_object_list(obj, src=r)
+            h = obj[0]
+    return h
+
+
+def exp3(a, cfg) -> list:
+    world, rank, dist = _dist()
+    device = int(os.environ.get("LOCAL_RANK", a.device))
+    recs = []
+    for name, kw, multi in CONSTRUCTS:
+        if world > 1 and not multi:
+            continue
+        if name == "gpu-redux-dsmem" and cfg.num_fish > 16384:
+            continue
+        try:
+            kw = dict(kw)
+            if kw.get("force_nccl") or (world > 1 and not kw.get("peer")):
+                uid = [sim.nccl_unique_id() if rank == 0 else None]
+                if dist is not None:
+                    dist.broadcast_object_list(uid, src=0)
+                kw["nccl_unique_id"] = uid[0]
+                kw["force_nccl"] = True
+            with sim.Engine(cfg, device=device, rank=rank, world_size=world, **kw) as eng:
+                if kw.get("peer") and world > 1:
+                    handles = [None] * world
+                    dist.all_gather_object(handles, eng.peer_handle())
+                    eng.peer_connect(handles)
+                for r in range(a.warmup + a.reps):
+                    _, _, t = eng.simulate(barycentre=False)
+                    if world > 1:  # the job's times: max over ranks
+                        tt = [None] * world
+                        dist.all_gather_object(tt, (t.seconds_total, t.seconds_eat))
+                        t.seconds_total = max(x[0] for x in tt)
+                        t.seconds_eat = max(x[1] for x in tt)
+                    h = _chained_checksum(eng, world, rank, dist)
+                    if r >= a.warmup and rank == 0:
+                        recs.append(_record("gpu-exp3", eng, cfg, t, r - a.warmup, construct=name, gpus=world,
+                                            checksum=h))
+        except Exception as e:
+            sys.stderr.write(f"gpu-exp3 {name}: {e}\n")
+            if rank == 0:
+                recs.append(_failed("gpu-exp3", name, cfg, world))
+    return recs
+
+
 def cmd_gpuexp(a) -> int:
     cfg = _config(a)
     cfg.validate()
     recs = []
-    # (experiment, strategy, step kernel, CTAs per SM or None = automatic grid)
-    plans = [("gpu-stream", "stream", False, None), ("gpu-stream-bulk", "stream", True, None)]
-    if cfg.num_fish <= 16384:
-        plans.append(("gpu-persistent", "persistent", False, None))
-    # Exp 1 analogue (thread count): the CTA count of the step kernel, 1..8 per SM
-    plans += [("gpu-grid", "stream", False, k) for k in (1, 2, 4, 8)]
-    for name, strategy, bulk, per_sm in plans:
-        try:
-            with sim.Engine(cfg, device=a.device, strategy=strategy, bulk=bulk) as eng:
-                if per_sm:
-                    eng.set_grid(per_sm * _sms(a.device))
-                ctas, tpc = eng.grid()
-                threads = 1 if strategy == "persistent" else ctas * tpc
-                for r in range(a.warmup + a.reps):
-                    _, _, t = eng.simulate(barycentre=False)
-                    if r >= a.warmup:
-                        recs.append(_record(name, strategy, cfg, eng, t, r - a.warmup, threads))
-        except Exception as e:  # bench.hpp:182-188: a failed cell becomes a NaN row
-            sys.stderr.write(f"{name}: {e}\n")
-            recs.append(records.BenchRecord(name, 1, strategy, cfg.num_fish, "gpu", 0, cfg.num_fish,
-                                            cfg.num_steps, math.nan, math.nan, 0))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.exp in ("1", "all") and world == 1:
+        recs += exp1(a, cfg)
+    if a.exp in ("3", "all"):
+        recs += exp3(a, cfg)
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
     return _emit(recs, a.out, sys.stderr)
 
 
@@ -117,8 +225,9 @@ def main(argv=None) -> int:
         p.add_argument("--device", type=int, default=0)
         p.add_argument("--out", default="")
         if name == "simulate":
-            p.add_argument("--strategy", default="auto", choices=["auto", "stream", "persistent"])
+            p.add_argument("--strategy", default="auto", choices=["auto", "stream", "persistent", "grid"])
         else:
+            p.add_argument("--exp", default="all", choices=["1", "3", "all"])
             p.add_argument("--reps", type=int, default=5)
             p.add_argument("--warmup", type=int, default=1)
     try:

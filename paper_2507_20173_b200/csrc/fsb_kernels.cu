@@ -35,6 +35,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef FSB_SPIN_ACQ
+#define FSB_SPIN_ACQ 0  // A/B: acquire load on every poll of a counter barrier
+#endif
+
 namespace fsb_dev {
 
 namespace {
@@ -217,10 +221,24 @@ __device__ __forceinline__ void red_add_release_gpu(unsigned long long* p, unsig
     asm volatile("red.add.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+
+// Spin with relaxed polls (no fence per poll) until *p >= target, then one
+// acquire fence: the arrivals' releases synchronise with it.
+__device__ __forceinline__ void spin_until_gpu(const unsigned long long* p, unsigned long long target) {
+    while (FSB_SPIN_ACQ ? ld_acquire_gpu(p) < target : ld_relaxed_gpu(p) < target) {
+    }
+    if (!FSB_SPIN_ACQ) asm volatile("fence.acquire.gpu;" ::: "memory");
 }
 
 // Peer exchange, producer side (warp 0 of the last CTA): the rank partial into
@@ -416,19 +434,22 @@ struct SoA2 {
 // then are the fish folded into the thread partial.  kSane: the state is in
 // range (fsb_math.cuh "In-range mode"); the eat divisor -- the global max,
 // which other ranks' states feed -- is range-checked here, once per call.
-template <bool kExplicitCur, int U, bool kSane, bool kRngFirst = false>
+// kPre: H[2u + f] holds fold_in(seed, fish) of pair u's fish f (the
+// step-independent RNG prefix, kept by the caller); the draws are made first as
+// with kRngFirst, without its scheduling fence.
+template <bool kExplicitCur, int U, bool kSane, bool kRngFirst = false, bool kPre = false>
 __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], double2 (&W)[U],
                                             double2 (&Q)[U], const double2 (&C)[U], const bool (&valid)[U],
                                             const SoA2& src, const uint64_t (&k)[U], const uint64_t (&gi)[U],
                                             const StepParams& P, bool eat, const SharedDivisor& M,
-                                            uint64_t step, Partial& acc) {
+                                            uint64_t step, Partial& acc, const uint64_t* H = nullptr) {
     bool ok[U];
     double n0[U], n1[U];
     bool all_ok = true;
     // M.b in [2^-506, 2^502] (positive: as an integer range on its bits)
     const uint64_t mb = static_cast<uint64_t>(__double_as_longlong(M.b));
     const bool ok0 = !kSane || !eat || (mb - 0x2050000000000000ull <= 0x3F00000000000000ull);
-    if (kRngFirst) {
+    if (kRngFirst || kPre) {
         // Every fish's units first: they depend on (seed, fish, step) only, so the
         // chains run while the state loads are in flight.  The loaded values then
         // pass through a fake dependency on the last draws (high word | (bits &
@@ -442,7 +463,7 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
         for (int u = 0; u < U; ++u) {
 #pragma unroll
             for (int f = 0; f < 2; ++f) {
-                const uint64_t h_step = fold_in(fold_in(P.seed, gi[u] + f), step);
+                const uint64_t h_step = fold_in(kPre ? H[2 * u + f] : fold_in(P.seed, gi[u] + f), step);
                 const uint64_t b0 = fold_in(h_step, 0);
                 const uint64_t b1 = fold_in(h_step, 1);
                 U0[u][f] = __ull2double_rn(b0 >> 11);
@@ -450,7 +471,7 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
                 dep |= static_cast<unsigned>(b1);
             }
         }
-        dep &= static_cast<unsigned>(P.zero);
+        dep = kPre ? 0u : (dep & static_cast<unsigned>(P.zero));
         // the fence goes into high words (one LOP3 each)
         auto fenced = [dep](double v) {
             return __hiloint2double(__double2hiint(v) | static_cast<int>(dep), __double2loint(v));
@@ -1508,6 +1529,18 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(con
 // No clusters: a plain cooperative launch, which Nsight Compute can replay (it
 // terminates the process on cooperative launches of clusters).
 constexpr unsigned kSGridMaxGrid = 160;  // warp 0 folds <= 5 partials per lane
+#ifndef FSB_SGRID_PAIRS
+#define FSB_SGRID_PAIRS 8
+#endif
+#ifndef FSB_SGRID_U
+#define FSB_SGRID_U 1
+#endif
+constexpr int kSGridPairs = FSB_SGRID_PAIRS;  // pairs per thread: pair_cap <= kSGridThreads * kSGridPairs
+constexpr int kSGridU = FSB_SGRID_U;          // pairs per pass (independent chains per thread)
+#ifndef FSB_SGRID_PRE
+#define FSB_SGRID_PRE 1
+#endif
+constexpr bool kSGridPre = FSB_SGRID_PRE;     // keep fold_in(seed, fish) of the thread's pairs in registers
 
 template <bool kSane, bool kBary>
 __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs g) {
@@ -1523,7 +1556,8 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
     const uint64_t npairs = a.n >> 1;
     const uint64_t plo = npairs * blockIdx.x / gridDim.x;
     const unsigned cnt = (unsigned)(npairs * (blockIdx.x + 1) / gridDim.x - plo);
-    FSB_CHECK(cnt <= g.pair_cap && gridDim.x <= kSGridMaxGrid);
+    FSB_CHECK(cnt <= g.pair_cap && g.pair_cap <= (unsigned)(kSGridThreads * kSGridPairs) &&
+              gridDim.x <= kSGridMaxGrid);
     double2* sx = sg_smem;
     double2* sy = sx + g.pair_cap;
     double2* sw = sy + g.pair_cap;
@@ -1546,6 +1580,17 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
         tail[2] = a.s.w[i];
         tail[3] = a.s.p[i];
     }
+    // the step-independent RNG prefix fold_in(seed, fish) (rng.hpp:35) of this
+    // thread's pairs, kept in registers for all steps: one fold_in of four per
+    // fish-update saved (there is no shared memory left to keep it in)
+    uint64_t H[kSGridPre ? kSGridPairs : 1][2];
+#pragma unroll
+    for (int j = 0; j < (kSGridPre ? kSGridPairs : 0); ++j) {
+        const unsigned q = t + j * kSGridThreads;
+        const uint64_t gi = a.gfirst + 2 * (plo + q);
+        H[j][0] = q < cnt ? fold_in(P.seed, gi) : 0ull;
+        H[j][1] = q < cnt ? fold_in(P.seed, gi + 1) : 0ull;
+    }
     if (t == 0) ecl = 0;
     eclk_bracket(g.eclk, false);
     __syncthreads();
@@ -1557,20 +1602,36 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
         const bool eat = prev_best > 0.0;
         const SharedDivisor M = make_divisor(eat ? prev_best : 1.0);
         Partial acc = identity();
-        for (unsigned q = t; q < cnt; q += blockDim.x) {
-            double2 X[1], Y[1], W[1], Q[1], C[1];
-            const bool valid[1] = {true};
-            const uint64_t qs[1] = {q};
-            const uint64_t gi[1] = {a.gfirst + 2 * (plo + q)};
-            X[0] = sx[q];
-            Y[0] = sy[q];
-            W[0] = sw[q];
-            Q[0] = sp[q];
-            fused_pairs<false, 1, kSane>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
-            sx[q] = X[0];
-            sy[q] = Y[0];
-            sw[q] = W[0];
-            sp[q] = Q[0];
+#pragma unroll
+        for (int j = 0; j < kSGridPairs; j += kSGridU) {  // kSGridU pairs per pass: independent fish chains
+            const unsigned q0 = t + j * kSGridThreads;
+            if (q0 < cnt) {
+                double2 X[kSGridU], Y[kSGridU], W[kSGridU], Q[kSGridU], C[kSGridU];
+                bool valid[kSGridU];
+                uint64_t qs[kSGridU], gi[kSGridU];
+#pragma unroll
+                for (int u = 0; u < kSGridU; ++u) {
+                    const unsigned q = q0 + u * kSGridThreads;
+                    valid[u] = q < cnt;
+                    qs[u] = valid[u] ? q : q0;
+                    gi[u] = a.gfirst + 2 * (plo + q);
+                    X[u] = sx[qs[u]];
+                    Y[u] = sy[qs[u]];
+                    W[u] = sw[qs[u]];
+                    Q[u] = sp[qs[u]];
+                }
+                fused_pairs<false, kSGridU, kSane, false, kSGridPre>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M,
+                                                                     step, acc, &H[kSGridPre ? j : 0][0]);
+#pragma unroll
+                for (int u = 0; u < kSGridU; ++u) {
+                    if (valid[u]) {
+                        sx[qs[u]] = X[u];
+                        sy[qs[u]] = Y[u];
+                        sw[qs[u]] = W[u];
+                        sp[qs[u]] = Q[u];
+                    }
+                }
+            }
         }
         if (has_tail && t == 0) {
             double x = tail[0], y = tail[1], w = tail[2], p = tail[3];
@@ -1587,8 +1648,7 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
             if (t == 0) {
                 store_partial(&slots[blockIdx.x], blk);
                 red_add_release_gpu(g.gen, 1ull);
-                while (ld_acquire_gpu(g.gen) < target) {
-                }
+                spin_until_gpu(g.gen, target);
             }
             __syncthreads();
             if (t < 32) {
@@ -1620,8 +1680,7 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
                 unsigned long long* slot = g.keys + k % 3;
                 red_max_relaxed_gpu(slot, key);
                 red_add_release_gpu(g.gen, 1ull);  // orders the red.max before the arrival
-                while (ld_acquire_gpu(g.gen) < target) {
-                }
+                spin_until_gpu(g.gen, target);
                 const double m = key_value(*reinterpret_cast<volatile unsigned long long*>(slot));
                 // slot (k+2)%3 was last read at step k-1 by every CTA (all arrived at k since):
                 // clear it for step k+2; this CTA's arrival at k+1 (release) publishes the clear
@@ -1838,7 +1897,8 @@ unsigned sgrid_pair_capacity(int device, int* grid) {
         return 0;
     }
     if (grid) *grid = num_sms(device);
-    return (unsigned)(dyn / 64);
+    const size_t cap = dyn / 64;
+    return (unsigned)(cap < (size_t)kSGridThreads * kSGridPairs ? cap : (size_t)kSGridThreads * kSGridPairs);
 }
 
 cudaError_t launch_sgrid_run(const SGridArgs& g, int grid, cudaStream_t st) {

@@ -243,11 +243,14 @@ struct CGridArgs {
 };
 
 // Shared-memory-resident persistent run (FSB_STRATEGY_GRID for schools that
-// fit on chip, ~1.06e6 fish on 148 SMs): one 1024-thread CTA per SM, the CTA's
+// fit on chip, ~1.06e6 fish on 148 SMs): one 512-thread CTA per SM, the CTA's
 // contiguous range of fish pairs held in shared memory for all num_steps steps,
 // one cooperative launch (no clusters: Nsight Compute can replay it); the CTAs
 // meet at a counter barrier each step.
-constexpr int kSGridThreads = 1024;
+#ifndef FSB_SGRID_THREADS
+#define FSB_SGRID_THREADS 512
+#endif
+constexpr int kSGridThreads = FSB_SGRID_THREADS;
 struct SGridArgs {
     StepArgs base;                // state (read at launch, written back at the end), scalars, n, gfirst
     uint64_t first_step;

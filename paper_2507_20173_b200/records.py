@@ -3,11 +3,24 @@
 Mirrors fsb::BenchRecord (bench.hpp:49-75) and the CSV format of csv.hpp:
 header kCsvHeader (csv.hpp:23-24), seconds with 9 significant digits and NaN
 for failed cells (csv.hpp:30-36), checksum as 16 lowercase hex digits
-(csv.hpp:38-42).  GPU rows use construct="gpu", threads = number of GPUs,
-schedule = the step-loop strategy ("graph" or "cluster") and chunk = fish per
-GPU, so the reference's own read_csv / validate_records / report charts
-accept them next to its CPU rows (tests/test_records.py checks this with the
-reference's csv.hpp).
+(csv.hpp:38-42).  GPU rows fill the columns as follows:
+  * threads      = number of GPUs (the team that runs the construct, where
+                   the reference has OpenMP threads);
+  * schedule     = the step loop the engine executed: "graph" (CUDA graph of
+                   step kernels), "grid" (one cooperative grid for all steps),
+                   "cluster" (one thread-block cluster for all steps);
+  * chunk        = fish per GPU thread of the step kernel's grid
+                   (fish / (GPUs x CTAs x threads per CTA)) -- the gpu-exp1
+                   sweep's axis;
+  * construct    = "gpu" (simulate), or the reduction construct of the global
+                   max in the gpu-exp3 rows (gpu-lastcta, gpu-nccl, gpu-peer,
+                   gpu-smem-counter, gpu-cluster-slots, gpu-flat-counter,
+                   gpu-redux-dsmem);
+  * seconds_eat  = SimResult::seconds_eat: the max region only, measured on
+                   the device (include/fsb_b200.h fsb_timing).
+The reference's own read_csv / validate_records / report charts accept them
+next to its CPU rows (tests/test_records.py checks this with the reference's
+csv.hpp).
 """
 from __future__ import annotations
 

@@ -605,10 +605,29 @@ def test_cli_simulate_record(tmp_path, capsys):
     assert recs[0].construct == "gpu" and recs[0].seconds_eat <= recs[0].seconds_total
     assert cli_main(["gpuexp", "--fish", "4096", "--steps", "50", "--reps", "2", "--warmup", "1",
                      "--out", str(out)]) == 0
-    recs = records.read_csv(out.read_text())
-    assert len(recs) == 14 and len({r.checksum for r in recs}) == 1 and not any(r.failed() for r in recs)
-    grid = [r for r in recs if r.experiment == "gpu-grid"]
-    assert len({r.threads for r in grid}) == 4  # 1, 2, 4, 8 CTAs per SM
+    text = out.read_text()
+    recs = records.read_csv(text)
+    assert len({r.checksum for r in recs}) == 1 and not any(r.failed() for r in recs)
+    exp1 = [r for r in recs if r.experiment == "gpu-exp1"]
+    assert len(exp1) == 14 and len({r.chunk for r in exp1}) >= 5  # the fish-per-thread axis
+    exp3 = [r for r in recs if r.experiment == "gpu-exp3"]
+    assert {r.construct for r in exp3} == {"gpu-lastcta", "gpu-nccl", "gpu-peer", "gpu-smem-counter",
+                                          "gpu-cluster-slots", "gpu-flat-counter", "gpu-redux-dsmem"}
+    assert len(exp3) == 14 and all(r.threads == 1 for r in exp3)
+    assert {r.schedule for r in exp3} == {"graph", "grid", "cluster"}
+    # Exp 3 rows carry a measured eat region (bench.hpp:132-148), valid for the reference's validate_records
+    assert all(0.0 < r.seconds_eat < r.seconds_total for r in recs)
+    ref = os.path.join(ROOT, "oracle", "_ref", "libfsbref.so")
+    if os.path.exists(ref):
+        import ctypes
+
+        L = oracle.Reference().L
+        L.ref_read_csv.restype = ctypes.c_int
+        L.ref_read_csv.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.c_char_p, ctypes.c_int]
+        issues = ctypes.c_int(-1)
+        err = ctypes.create_string_buffer(256)
+        assert L.ref_read_csv(text.encode(), ctypes.byref(issues), err, 256) == len(recs), err.value
+        assert issues.value == 0
 
 
 def test_gather_matches_download(orc):

@@ -68,6 +68,15 @@ VARIANTS = {
     "d576x2": ["-DFSB_DYN_THREADS=576", "-DFSB_DYN_MIN_BLOCKS=2"],
     "d384x3": ["-DFSB_DYN_THREADS=384", "-DFSB_DYN_MIN_BLOCKS=3"],
     "d640x2": ["-DFSB_DYN_THREADS=640", "-DFSB_DYN_MIN_BLOCKS=2"],
+    # shared-memory grid kernel: threads per CTA x pairs per thread (x pairs per pass)
+    "sg768": ["-DFSB_SGRID_THREADS=768", "-DFSB_SGRID_PAIRS=5"],
+    "sg512u2": ["-DFSB_SGRID_THREADS=512", "-DFSB_SGRID_PAIRS=8", "-DFSB_SGRID_U=2"],
+    "sg1024": ["-DFSB_SGRID_THREADS=1024", "-DFSB_SGRID_PAIRS=4"],
+    "spinacq": ["-DFSB_SPIN_ACQ=1"],
+    "sg512u2np": ["-DFSB_SGRID_U=2", "-DFSB_SGRID_PRE=0"],
+    "sg512np": ["-DFSB_SGRID_PRE=0"],
+    "sg1024np": ["-DFSB_SGRID_THREADS=1024", "-DFSB_SGRID_PAIRS=4", "-DFSB_SGRID_PRE=0"],
+    "sg768u2np": ["-DFSB_SGRID_THREADS=768", "-DFSB_SGRID_PAIRS=5", "-DFSB_SGRID_U=2", "-DFSB_SGRID_PRE=0"],
     # claimed-tile kernel: minimum 32-pair groups per tile
     "dg1": ["-DFSB_DYN_MIN_GROUPS=1"],
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
