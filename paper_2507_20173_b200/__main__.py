@@ -63,7 +63,7 @@ def _record(experiment, eng, cfg, t, rep, construct="gpu", gpus=1, gpu_threads=N
         ctas, tpc = eng.grid()
         gpu_threads = ctas * tpc
     return records.BenchRecord(experiment=experiment, threads=gpus, schedule=SCHEDULE.get(used, used),
-                               chunk=max(1, cfg.num_fish // max(1, gpus * gpu_threads)), construct=construct,
+                               chunk=max(1, -(-cfg.num_fish // max(1, gpus * gpu_threads))), construct=construct,
                                rep=rep, fish=cfg.num_fish, steps=cfg.num_steps, seconds_total=t.seconds_total,
                                seconds_eat=t.seconds_eat,
                                checksum=eng.checksum() if checksum is None else checksum)

@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 #include <cstdlib>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -271,6 +272,18 @@ bool co_schedule_refused(cudaError_t ce) {
            ce == cudaErrorNotPermitted;
 }
 
+// NVTX ranges around every public entry point (tracing): an
+// nsys / ncu --nvtx timeline shows init / upload / run / move / eat / download
+// per rank.  Header-only NVTX v3: without an attached tool a range is one
+// predicted branch.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define FSB_NVTX(name) NvtxRange fsb_nvtx_range_(name)
+
 int guard(fsb_engine* e) {
     if (!e) return fail(FSB_ERR_INVALID_ARGUMENT, "null engine");
     CU(cudaSetDevice(e->device));
@@ -474,6 +487,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
 
 int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
                double* seconds) {
+    FSB_NVTX("run_stream: graph of fused step kernels");
     const auto key = std::make_pair(T, (e->cur_explicit ? 1 : 0) | (in_range(e) ? 2 : 0));
     auto it = e->graphs.find(key);
     if (it == e->graphs.end()) {
@@ -519,6 +533,7 @@ size_t cl_slot_bytes(const fsb_engine* e) {
 }
 
 int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary, double* seconds) {
+    FSB_NVTX("run_grid: cooperative grid kernel");
     if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode)
         return fail(FSB_ERR_UNSUPPORTED, "grid strategy: single rank, compact state only");
     TRY(ensure_run_buffers(e, T));
@@ -599,6 +614,7 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
 
 int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
                    double* seconds) {
+    FSB_NVTX("run_persistent: persistent cluster kernel");
     if (T > e->cl_cap) {
         if (e->d_cl_trace) cudaFree(e->d_cl_trace);
         if (e->d_cl_bary) cudaFree(e->d_cl_bary);
@@ -950,6 +966,7 @@ int fsb_engine_shard(const fsb_engine* e, uint64_t* first, uint64_t* count) {
 }
 
 int fsb_engine_init(fsb_engine* e) {
+    FSB_NVTX("fsb_engine_init");
     TRY(guard(e));
     fsb_dev::InitArgs a{};
     a.s = e->s;
@@ -966,6 +983,7 @@ int fsb_engine_init(fsb_engine* e) {
 }
 
 int fsb_engine_upload(fsb_engine* e, const fsb_fish* fish, uint64_t count) {
+    FSB_NVTX("fsb_engine_upload");
     TRY(guard(e));
     if (count != e->count) return fail(FSB_ERR_INVALID_ARGUMENT, "upload count != shard count");
     if (count && !fish) return fail(FSB_ERR_INVALID_ARGUMENT, "null fish");
@@ -1014,6 +1032,7 @@ int fsb_engine_upload(fsb_engine* e, const fsb_fish* fish, uint64_t count) {
 }
 
 int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count) {
+    FSB_NVTX("fsb_engine_download");
     TRY(guard(e));
     if (count != e->count) return fail(FSB_ERR_INVALID_ARGUMENT, "download count != shard count");
     if (count && !fish) return fail(FSB_ERR_INVALID_ARGUMENT, "null fish");
@@ -1050,6 +1069,7 @@ int fsb_engine_download(fsb_engine* e, fsb_fish* fish, uint64_t count) {
 }
 
 int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
+    FSB_NVTX("fsb_engine_move");
     TRY(guard(e));
     TRY(need_peers(e));
     CU(cudaEventRecord(e->ev0, e->stream));
@@ -1078,6 +1098,7 @@ int fsb_engine_move(fsb_engine* e, uint64_t step, double* seconds) {
 }
 
 int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
+    FSB_NVTX("fsb_engine_eat");
     TRY(guard(e));
     TRY(need_peers(e));
     CU(cudaMemsetAsync(&e->eclk->ns, 0, sizeof(unsigned long long), e->stream));
@@ -1128,6 +1149,7 @@ int run_stream_chunked(fsb_engine* e, uint64_t first_step, uint64_t T, double* t
 
 int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, double* trace, double* bary,
                    fsb_timing* timing) {
+    FSB_NVTX("fsb_engine_run");
     TRY(guard(e));
     TRY(need_peers(e));
     TRY(phase_only(e, "fsb_engine_run"));
@@ -1177,6 +1199,7 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
 }
 
 int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* timing) {
+    FSB_NVTX("fsb_engine_simulate");
     TRY(guard(e));
     TRY(phase_only(e, "fsb_engine_simulate"));
     CU(cudaEventRecord(e->ev0, e->stream));
@@ -1190,6 +1213,7 @@ int fsb_engine_simulate(fsb_engine* e, double* trace, double* bary, fsb_timing* 
 }
 
 int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
+    FSB_NVTX("fsb_engine_barycentre");
     TRY(guard(e));
     TRY(need_peers(e));
     if (!e->max_valid || !e->sums_valid) TRY(reduce_current(e));
@@ -1209,6 +1233,7 @@ int fsb_engine_barycentre(fsb_engine* e, double sums[3], double xy[2]) {
 }
 
 int fsb_engine_partial(fsb_engine* e, double out[5]) {
+    FSB_NVTX("fsb_engine_partial");
     TRY(guard(e));
     TRY(need_peers(e));
     if (!out) return fail(FSB_ERR_INVALID_ARGUMENT, "null out");
@@ -1225,6 +1250,7 @@ int fsb_engine_partial(fsb_engine* e, double out[5]) {
 }
 
 int fsb_engine_set_partials(fsb_engine* e, const double* parts, size_t count) {
+    FSB_NVTX("fsb_engine_set_partials");
     TRY(guard(e));
     if (!e->host_xchg) return fail(FSB_ERR_INVALID_ARGUMENT, "set_partials needs FSB_FLAG_HOST_EXCHANGE");
     if (!parts || count != 5 * (size_t)e->world)
@@ -1254,6 +1280,7 @@ int fsb_engine_set_partials(fsb_engine* e, const double* parts, size_t count) {
 }
 
 int fsb_engine_gather(fsb_engine* e, const uint64_t* local_idx, uint64_t n, fsb_fish* out) {
+    FSB_NVTX("fsb_engine_gather");
     TRY(guard(e));
     if (n && (!local_idx || !out)) return fail(FSB_ERR_INVALID_ARGUMENT, "null argument");
     for (uint64_t k = 0; k < n; ++k)
@@ -1275,6 +1302,7 @@ int fsb_engine_gather(fsb_engine* e, const uint64_t* local_idx, uint64_t n, fsb_
 }
 
 int fsb_engine_checksum(fsb_engine* e, uint64_t h_in, uint64_t* h_out) {
+    FSB_NVTX("fsb_engine_checksum");
     TRY(guard(e));
     if (!h_out) return fail(FSB_ERR_INVALID_ARGUMENT, "null h_out");
     TRY(ensure_staging(e));

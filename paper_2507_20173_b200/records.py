@@ -10,7 +10,7 @@ for failed cells (csv.hpp:30-36), checksum as 16 lowercase hex digits
                    step kernels), "grid" (one cooperative grid for all steps),
                    "cluster" (one thread-block cluster for all steps);
   * chunk        = fish per GPU thread of the step kernel's grid
-                   (fish / (GPUs x CTAs x threads per CTA)) -- the gpu-exp1
+                   (fish / (GPUs x CTAs x threads per CTA), rounded up) -- the gpu-exp1
                    sweep's axis;
   * construct    = "gpu" (simulate), or the reduction construct of the global
                    max in the gpu-exp3 rows (gpu-lastcta, gpu-nccl, gpu-peer,

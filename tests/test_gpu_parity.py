@@ -579,6 +579,21 @@ def test_cpp_dropin_suite():
     assert "0 failures" in r.stdout
 
 
+def test_cpp_dropin_reference_types():
+    """tests/cpp/test_dropin_reftypes: INTEGRATION.md section 1 as a reference user
+    writes it -- the reference's own fsb/sim.hpp types (FSB_GPU_USE_REFERENCE_TYPES)
+    through fsb::gpu, checked against the reference's parfor path: init_school,
+    move/eat step by step, test_sim.cpp:217-225 and acceptance.cpp:63-102
+    criterion 1 for every GPU strategy.  Built where /root/reference exists
+    (build()); the binary travels to the GPU box."""
+    exe = os.path.join(ROOT, "tests", "cpp", "test_dropin_reftypes")
+    if not os.path.exists(exe):
+        pytest.skip("built only where the reference headers exist (run build() in the dev container)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "4 cases, 0 failed" in r.stdout, r.stdout
+
+
 def test_fast_math_selftest():
     """The guarded fast fp64 paths of the step kernel equal __ddiv_rn / __dsqrt_rn
     bit-for-bit on 2^27 operands (raw bit patterns incl. NaN/inf/subnormals, and
@@ -603,13 +618,18 @@ def test_cli_simulate_record(tmp_path, capsys):
     recs = records.read_csv(out.read_text())
     assert len(recs) == 1 and recs[0].checksum == 0xF7E6675CBE28EB38
     assert recs[0].construct == "gpu" and recs[0].seconds_eat <= recs[0].seconds_total
-    assert cli_main(["gpuexp", "--fish", "4096", "--steps", "50", "--reps", "2", "--warmup", "1",
+    # Exp 1 at 2e6 fish: 1/8 of the SMs .. 8 CTAs per SM spans 6..434 fish per thread
+    assert cli_main(["gpuexp", "--exp", "1", "--fish", "2000000", "--steps", "10", "--reps", "2", "--warmup", "1",
+                     "--out", str(out)]) == 0
+    exp1 = records.read_csv(out.read_text())
+    assert len({r.checksum for r in exp1}) == 1 and not any(r.failed() for r in exp1)
+    assert len(exp1) == 14 and len({r.chunk for r in exp1}) >= 5  # the fish-per-thread axis
+    assert all(r.experiment == "gpu-exp1" and r.schedule == "graph" for r in exp1)
+    assert cli_main(["gpuexp", "--exp", "3", "--fish", "4096", "--steps", "50", "--reps", "2", "--warmup", "1",
                      "--out", str(out)]) == 0
     text = out.read_text()
     recs = records.read_csv(text)
     assert len({r.checksum for r in recs}) == 1 and not any(r.failed() for r in recs)
-    exp1 = [r for r in recs if r.experiment == "gpu-exp1"]
-    assert len(exp1) == 14 and len({r.chunk for r in exp1}) >= 5  # the fish-per-thread axis
     exp3 = [r for r in recs if r.experiment == "gpu-exp3"]
     assert {r.construct for r in exp3} == {"gpu-lastcta", "gpu-nccl", "gpu-peer", "gpu-smem-counter",
                                           "gpu-cluster-slots", "gpu-flat-counter", "gpu-redux-dsmem"}
