@@ -380,7 +380,7 @@ def run_ours(args, world, rank, local):
         uid = fsb.nccl_unique_id()
     eng = fsb.Engine(cfg, device=local, rank=rank, world_size=world, nccl_unique_id=uid,
                      strategy=args.strategy, alternate=not args.no_alternate, bulk=args.bulk,
-                     force_nccl=args.force_nccl, peer=args.peer)
+                     force_nccl=args.force_nccl, peer=args.peer, ws_tiles=args.ws)
     if args.peer and world > 1:
         import torch.distributed as dist
 
@@ -408,7 +408,8 @@ def run_ours(args, world, rank, local):
     peak_gbs, peak_src = peaks()
     achieved = BYTES_PER_UPDATE * n_local / kernel_s / 1e9
     _, cta_threads = eng.grid()
-    kernel = "step_kernel_bulk" if args.bulk else ("step_kernel" if cta_threads == 256 else "step_kernel_dyn")
+    kernel = ("step_kernel_bulk" if args.bulk else "step_kernel_ws" if args.ws
+              else ("step_kernel" if cta_threads == 256 else "step_kernel_dyn"))
     traffic, traffic_src = load_profile_traffic(n_local, kernel)
     same_bytes = same_bytes_memory_bound(n_local * MOVED_BYTES_PER_UPDATE // 2, local)
 
@@ -528,6 +529,8 @@ def main():
                     help="fixed tile order (default reverses odd steps to reuse L2 across steps)")
     ap.add_argument("--bulk", action="store_true",
                     help="cp.async.bulk shared-memory ring step kernel instead of the LDG one (A/B)")
+    ap.add_argument("--ws", action="store_true",
+                    help="warp-specialised step kernel (TMA producer warp + 31 consumer warps per SM; A/B)")
     ap.add_argument("--force-nccl", action="store_true",
                     help="exercise the NCCL exchange path even on one rank (testing)")
     ap.add_argument("--peer", action="store_true",

@@ -437,19 +437,59 @@ struct SoA2 {
 // kPre: H[2u + f] holds fold_in(seed, fish) of pair u's fish f (the
 // step-independent RNG prefix, kept by the caller); the draws are made first as
 // with kRngFirst, without its scheduling fence.
-template <bool kExplicitCur, int U, bool kSane, bool kRngFirst = false, bool kPre = false>
+// Pair u's two draws as the 53-bit integers of swim_units_guarded: fish 2u+f
+// of the call draws (U0[u][f], U1[u][f]).
+template <int U>
+struct PairDraws {
+    double U0[U][2], U1[U][2];
+};
+
+template <int U>
+__device__ __forceinline__ void draw_pairs(PairDraws<U>& d, const uint64_t (&gi)[U], uint64_t seed, uint64_t step) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            const uint64_t h_step = fold_in(fold_in(seed, gi[u] + f), step);
+            d.U0[u][f] = __ull2double_rn(fold_in(h_step, 0) >> 11);
+            d.U1[u][f] = __ull2double_rn(fold_in(h_step, 1) >> 11);
+        }
+    }
+}
+
+// kDrawn: DR holds the pairs' draws, made by the caller ahead of the state
+// (step_kernel_ws draws before it waits for the stage to land).
+template <bool kExplicitCur, int U, bool kSane, bool kRngFirst = false, bool kPre = false, bool kDrawn = false>
 __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], double2 (&W)[U],
                                             double2 (&Q)[U], const double2 (&C)[U], const bool (&valid)[U],
                                             const SoA2& src, const uint64_t (&k)[U], const uint64_t (&gi)[U],
                                             const StepParams& P, bool eat, const SharedDivisor& M,
-                                            uint64_t step, Partial& acc, const uint64_t* H = nullptr) {
+                                            uint64_t step, Partial& acc, const uint64_t* H = nullptr,
+                                            const PairDraws<U>* DR = nullptr) {
     bool ok[U];
     double n0[U], n1[U];
     bool all_ok = true;
     // M.b in [2^-506, 2^502] (positive: as an integer range on its bits)
     const uint64_t mb = static_cast<uint64_t>(__double_as_longlong(M.b));
     const bool ok0 = !kSane || !eat || (mb - 0x2050000000000000ull <= 0x3F00000000000000ull);
-    if (kRngFirst || kPre) {
+    if (kDrawn) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ok[u] = ok0;
+            if (valid[u]) {
+                const double c0 = kExplicitCur ? C[u].x : objective_guarded<kSane>(X[u].x, Y[u].x, P.half_pond, ok[u]);
+                const double c1 = kExplicitCur ? C[u].y : objective_guarded<kSane>(X[u].y, Y[u].y, P.half_pond, ok[u]);
+                double w0 = W[u].x, w1 = W[u].y;
+                if (eat) w0 = eat_weight_guarded<kSane>(w0, Q[u].x, c0, M, P.w_max, ok[u]);
+                if (eat) w1 = eat_weight_guarded<kSane>(w1, Q[u].y, c1, M, P.w_max, ok[u]);
+                W[u] = make_double2(w0, w1);
+                n0[u] = swim_units_guarded<kSane>(X[u].x, Y[u].x, w0, DR->U0[u][0], DR->U1[u][0], P, ok[u]);
+                n1[u] = swim_units_guarded<kSane>(X[u].y, Y[u].y, w1, DR->U0[u][1], DR->U1[u][1], P, ok[u]);
+                Q[u] = make_double2(c0, c1);
+                all_ok &= ok[u];
+            }
+        }
+    } else if (kRngFirst || kPre) {
         // Every fish's units first: they depend on (seed, fish, step) only, so the
         // chains run while the state loads are in flight.  The loaded values then
         // pass through a fake dependency on the last draws (high word | (bits &
@@ -1038,6 +1078,473 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
         }
     }
     grid_finish(acc, a.ws, a.part_out, a.px, a.world, a.ec.out);
+}
+
+// ---------------------------------------------------------------------------
+// step_kernel_ws: the fused step, warp-specialised.  One 1024-thread CTA per
+// SM: warp 0's elected lane is a producer that streams the CTA's state HBM ->
+// shared memory with cp.async.bulk into a ring of kWsRounds round buffers
+// (full/empty mbarrier each); warps 1..31 consume.  The shard's 32-pair
+// groups form stripes of 31 (one per consumer warp) dealt round-robin to the
+// CTAs (one moving front over the arrays, as step_kernel_dyn); in round r a
+// CTA takes its r-th stripe (its last first on odd steps: L2 reuse), which is
+// contiguous, so one round is four bulk copies of up to 15.5 KB (x, y, w, p)
+// and consumer warp c takes group c of it.  A consumer draws its pair's RNG
+// (seed, fish, step only) first, then waits for the round, copies its pair
+// into registers, releases the buffer at once and computes from registers,
+// storing the new state straight to HBM (STG).  The buffers are held only for
+// the four LDS, so the ring is almost entirely loads in flight -- up to
+// kWsRounds x 62 KB per SM, independent of the registers the step needs
+// (which cap the LDG kernels at 1024 resident threads and so their bytes in
+// flight).  Every warp's partial, and the fold of the 31 warp partials in
+// warp order, are fixed for a fixed (n, grid, step parity).
+#ifndef FSB_WS_ROUNDS
+#define FSB_WS_ROUNDS 3
+#endif
+#ifndef FSB_WS_EXP
+#define FSB_WS_EXP 0  // TEMP experiment: 1 memory only, 2 no loads, 3 no loads no stores
+#endif
+constexpr int kWsThreads = 1024;
+constexpr unsigned kWsConsumers = kWsThreads / 32 - 1;  // = groups per stripe
+constexpr unsigned kWsRounds = FSB_WS_ROUNDS;
+constexpr unsigned kWsPairs = kWsConsumers * 32;        // pairs per stripe
+struct WsRound {
+    double2 x[kWsPairs], y[kWsPairs], w[kWsPairs], p[kWsPairs];
+};
+constexpr size_t kWsSmemBytes = kWsRounds * sizeof(WsRound);
+
+// The shared-memory ring of the warp-specialised kernels.
+struct WsRing {
+    WsRound* buf;
+    uint64_t* full;
+    uint64_t* empty;
+};
+
+// Producer: round buffer b <- the stripe of pairs [q0, q0 + np) of x, y, w, p.
+__device__ __forceinline__ void ws_load(const StepArgs& a, const WsRing& R, unsigned b, uint64_t q0, unsigned np) {
+    const unsigned bytes = np * (unsigned)sizeof(double2);
+    FSB_CHECK(np >= 1 && np <= kWsPairs);
+    if (FSB_WS_EXP >= 2) {
+        mbar_arrive(&R.full[b]);
+        return;
+    }
+    mbar_expect_tx(&R.full[b], 4 * bytes);
+    bulk_load(R.buf[b].x, reinterpret_cast<const double2*>(a.s.x) + q0, bytes, &R.full[b]);
+    bulk_load(R.buf[b].y, reinterpret_cast<const double2*>(a.s.y) + q0, bytes, &R.full[b]);
+    bulk_load(R.buf[b].w, reinterpret_cast<const double2*>(a.s.w) + q0, bytes, &R.full[b]);
+    bulk_load(R.buf[b].p, reinterpret_cast<const double2*>(a.s.p) + q0, bytes, &R.full[b]);
+}
+
+// One consumer thread's pair of a round: fetched (draws first, then the stage),
+// then computed and stored.
+struct WsPair {
+    double2 X[1], Y[1], W[1], Q[1];
+    PairDraws<1> dr;
+    uint64_t q[1], gi[1];
+    bool valid[1];
+};
+
+// Consumer warp c: pair q = (first group of the stripe + c) x 32 + lane,
+// valid below `limit` pairs; round buffer b at parity ph.  Releases b.
+__device__ __forceinline__ void ws_fetch(WsPair& f, const StepArgs& a, const StepParams& P, uint64_t step,
+                                         const WsRing& R, unsigned b, unsigned ph, unsigned c, unsigned g,
+                                         uint64_t limit) {
+    const unsigned lane = threadIdx.x & 31;
+    f.q[0] = (uint64_t)(g + c) * 32 + lane;
+    f.valid[0] = f.q[0] < limit;
+    f.gi[0] = a.gfirst + 2 * f.q[0];
+    draw_pairs<1>(f.dr, f.gi, P.seed, step);
+    mbar_wait(&R.full[b], ph);
+    const unsigned k = c * 32 + lane;
+    if (f.valid[0]) {
+        f.X[0] = R.buf[b].x[k];
+        f.Y[0] = R.buf[b].y[k];
+        f.W[0] = R.buf[b].w[k];
+        f.Q[0] = R.buf[b].p[k];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&R.empty[b]);
+}
+
+// kFast: in-range mode with an in-range divisor -- fish_sane, no guard and no
+// fallback call in the loop (a call would make ptxas spill the loop's live
+// registers around it).
+template <bool kSane, bool kFast>
+__device__ __forceinline__ void ws_compute(WsPair& f, const StepArgs& a, const StepParams& P, bool eat,
+                                           const SharedDivisor& M, uint64_t step, Partial& acc) {
+    double2* X2 = reinterpret_cast<double2*>(a.s.x);
+    double2* Y2 = reinterpret_cast<double2*>(a.s.y);
+    double2* W2 = reinterpret_cast<double2*>(a.s.w);
+    double2* P2 = reinterpret_cast<double2*>(a.s.p);
+    if (FSB_WS_EXP == 1) {
+    } else if (kFast) {
+        if (f.valid[0]) {
+            const double n0 = fish_sane(f.X[0].x, f.Y[0].x, f.W[0].x, f.Q[0].x, eat, M, f.dr.U0[0][0],
+                                        f.dr.U1[0][0], P);
+            const double n1 = fish_sane(f.X[0].y, f.Y[0].y, f.W[0].y, f.Q[0].y, eat, M, f.dr.U0[0][1],
+                                        f.dr.U1[0][1], P);
+            accumulate(acc, f.X[0].x, f.Y[0].x, f.Q[0].x, n0);
+            accumulate(acc, f.X[0].y, f.Y[0].y, f.Q[0].y, n1);
+        }
+    } else {
+        const SoA2 src{X2, Y2, W2, P2, nullptr};
+        fused_pairs<false, 1, kSane, false, false, true>(f.X, f.Y, f.W, f.Q, f.X, f.valid, src, f.q, f.gi, P, eat, M,
+                                                         step, acc, nullptr, &f.dr);
+    }
+    if (f.valid[0] && FSB_WS_EXP != 3) {
+        const uint64_t q = f.q[0];
+        X2[q] = f.X[0];
+        Y2[q] = f.Y[0];
+        W2[q] = f.W[0];
+        P2[q] = f.Q[0];
+    }
+}
+
+// In-range state and an in-range divisor (the global max, which other ranks'
+// states feed: checked once per step) leave nothing to guard.
+template <bool kSane>
+__device__ __forceinline__ bool ws_fast(bool eat, const SharedDivisor& M) {
+    const uint64_t mb = static_cast<uint64_t>(__double_as_longlong(M.b));
+    return kSane && (!eat || mb - 0x2050000000000000ull <= 0x3F00000000000000ull);
+}
+
+template <bool kSane, bool kFast>
+__device__ __forceinline__ void ws_consume(const StepArgs& a, const StepParams& P, bool eat, const SharedDivisor& M,
+                                           uint64_t step, const WsRing& R, unsigned c, unsigned g0,
+                                           unsigned stride, unsigned rounds, Partial& acc) {
+    const uint64_t npairs = a.n >> 1;
+    const bool rev = a.alternate && (step & 1ull);
+    unsigned b = 0, ph = 0, g = g0;
+    for (unsigned r = 0; r < rounds; ++r) {
+        WsPair f;
+        ws_fetch(f, a, P, step, R, b, ph, c, g, npairs);
+        ws_compute<kSane, kFast>(f, a, P, eat, M, step, acc);
+        g = rev ? g - stride : g + stride;
+        if (++b == kWsRounds) {
+            b = 0;
+            ph ^= 1u;
+        }
+    }
+}
+
+template <bool kSane>
+__global__ void __launch_bounds__(kWsThreads, 1) step_kernel_ws(const StepArgs a) {
+    extern __shared__ __align__(128) unsigned char ws_smem[];
+    __shared__ __align__(8) uint64_t full[kWsRounds];
+    __shared__ __align__(8) uint64_t empty[kWsRounds];
+    __shared__ Partial warp_part[32];
+    const WsRing R{reinterpret_cast<WsRound*>(ws_smem), full, empty};
+
+    const StepParams P = params_of(a.k);
+    const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
+    const unsigned t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    if (t == 0) {
+        for (unsigned s = 0; s < kWsRounds; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWsConsumers);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_wait_and_release();
+    const Partial prev = combine_prev(a.part_in, a.world, a.px);
+    publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
+    const bool eat = prev.best > 0.0;  // sim.hpp:115
+    const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
+    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
+    const uint64_t n = a.n;
+    const uint64_t npairs = n >> 1;
+    const bool rev = a.alternate && (step & 1ull);
+
+    // 32-bit group indices: up to 2^37 fish per shard
+    const unsigned ngroups = (unsigned)((npairs + 31) / 32);
+    const unsigned nstripes = (ngroups + kWsConsumers - 1) / kWsConsumers;
+    const unsigned rounds = nstripes > blockIdx.x ? (nstripes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    // first group of round 0's stripe and the step between rounds' stripes
+    const unsigned stride = gridDim.x * kWsConsumers;
+    const unsigned g0 = (blockIdx.x + (rev && rounds ? (rounds - 1) * gridDim.x : 0u)) * kWsConsumers;
+    __syncthreads();  // barriers initialised
+
+    Partial acc = identity();
+    if (warp == 0) {
+        if (lane == 0) {
+            unsigned b = 0, ph = 0, g = g0;
+            for (unsigned r = 0; r < rounds; ++r) {
+                if (r >= kWsRounds) mbar_wait(&empty[b], ph ^ 1u);  // round r - kWsRounds consumed
+                const uint64_t q0 = (uint64_t)g * 32;                // the stripe is contiguous
+                ws_load(a, R, b, q0, (npairs - q0 < kWsPairs) ? (unsigned)(npairs - q0) : kWsPairs);
+                g = rev ? g - stride : g + stride;
+                if (++b == kWsRounds) {
+                    b = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else {
+        const unsigned c = warp - 1;
+        if (ws_fast<kSane>(eat, M))
+            ws_consume<kSane, true>(a, P, eat, M, step, R, c, g0, stride, rounds, acc);
+        else
+            ws_consume<kSane, false>(a, P, eat, M, step, R, c, g0, stride, rounds, acc);
+        acc = warp_reduce(acc);
+        if (lane == 0) warp_part[c] = acc;
+    }
+    __syncthreads();
+    const unsigned long long t_done = (a.ec.out && t == 0) ? gtimer() : 0ull;
+    Partial cta = identity();
+    if (warp == 0) {
+        if (lane < kWsConsumers) cta = warp_part[lane];
+        cta = warp_reduce(cta);
+        if ((n & 1ull) && blockIdx.x == 0 && t == 0) {  // odd tail fish
+            const uint64_t i = n - 1;
+            double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];
+            Partial tail = identity();
+            fused_fish(x, y, w, p, objective(x, y, P.half_pond), eat, M, a.gfirst + i, step, P, tail);
+            a.s.x[i] = x;
+            a.s.y[i] = y;
+            a.s.w[i] = w;
+            a.s.p[i] = p;
+            fold(cta, tail);
+        }
+    }
+    grid_publish(cta, a.ws, a.part_out, a.px, a.world, a.ec.out, t_done);
+}
+
+// ---------------------------------------------------------------------------
+// wgrid_kernel: all T steps of a single-rank school in ONE cooperative launch
+// of step_kernel_ws's warp specialisation (FSB_FLAG_WS_GRID).  Each CTA owns
+// one balanced contiguous chunk of 32-pair groups for the whole run, walked in
+// rounds of 31 groups (forwards on even steps, backwards on odd ones, so a
+// step's first rounds are the previous step's last, still in L2).  What the
+// persistent form removes from every step is the kernel boundary: the next
+// step's loads need only THIS CTA's stores of the previous step (the chunk is
+// its own), so the producer streams on as soon as the consumers have stored
+// and fenced their last round (a step-done mbarrier), while the consumers'
+// global max crosses the grid; the consumers meanwhile draw and fetch their
+// first round of the next step and only its arithmetic waits for the max.
+// Per step, consumer warp 0's lane 0 publishes the CTA partial (slot of step
+// parity), arrives on a grid counter and spins; the warp then folds all CTA
+// partials in index order (every CTA the same tree: bit-identical totals).
+// The explicit-cur state and multi-rank runs take the graph of step kernels;
+// the trailing eat is the engine's eat_kernel.
+
+#ifndef FSB_WGRID_STRIPED
+#define FSB_WGRID_STRIPED 1
+#endif
+#ifndef FSB_WGRID_TIMING
+#define FSB_WGRID_TIMING 0
+#endif
+#ifndef FSB_WGRID_RELAXED
+#define FSB_WGRID_RELAXED 0
+#endif
+#ifndef FSB_WGRID_NOPROXY
+#define FSB_WGRID_NOPROXY 0
+#endif
+constexpr unsigned kWGridMaxGrid = 160;  // consumer warp 0 folds <= 5 CTA partials per lane
+
+__device__ __forceinline__ void named_bar_sync(unsigned id, unsigned count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// One step of wgrid_kernel for consumer warp c: its group of every round of
+// the CTA's chunk (round 0 possibly fetched already), plus the school's odd
+// last fish (CTA 0, consumer warp 0, lane 0), all on the unguarded fast paths.
+__device__ __forceinline__ void wgrid_rounds(WsPair& f, bool have, const StepArgs& a, const StepParams& P, bool eat,
+                                             const SharedDivisor& M, uint64_t step, const WsRing& R, unsigned& b,
+                                             unsigned& ph, unsigned c, unsigned glo, unsigned gstride,
+                                             unsigned rounds, bool rev, uint64_t limit, Partial& acc) {
+    // stripe of round r: glo + r x gstride forwards, glo + (rounds - 1 - r) x gstride backwards
+    unsigned g = glo + (rev ? rounds - 1 : 0u) * gstride;
+    const unsigned d = rev ? 0u - gstride : gstride;
+    for (unsigned r = 0; r < rounds; ++r) {
+        if (r || !have) ws_fetch(f, a, P, step, R, b, ph, c, g, limit);
+        ws_compute<true, true>(f, a, P, eat, M, step, acc);
+        g += d;
+        if (++b == kWsRounds) {
+            b = 0;
+            ph ^= 1u;
+        }
+    }
+    if ((a.n & 1ull) && blockIdx.x == 0 && c == 0 && (threadIdx.x & 31) == 0) {  // the odd last fish (global)
+        const uint64_t i = a.n - 1;
+        double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];
+        const uint64_t h = fold_in(fold_in(P.seed, a.gfirst + i), step);
+        const double cn = fish_sane(x, y, w, p, eat, M, __ull2double_rn(fold_in(h, 0) >> 11),
+                                    __ull2double_rn(fold_in(h, 1) >> 11), P);
+        accumulate(acc, x, y, p, cn);
+        a.s.x[i] = x;
+        a.s.y[i] = y;
+        a.s.w[i] = w;
+        a.s.p[i] = p;
+    }
+}
+
+__global__ void __launch_bounds__(kWsThreads, 1) wgrid_kernel(const WGridArgs g) {
+    extern __shared__ __align__(128) unsigned char ws_smem[];
+    __shared__ __align__(8) uint64_t full[kWsRounds];
+    __shared__ __align__(8) uint64_t empty[kWsRounds];
+    __shared__ __align__(8) uint64_t stepdone;
+    __shared__ Partial warp_part[32];
+    __shared__ Partial shared_tot;
+    __shared__ unsigned long long ecl;  // eat-region SM cycles (consumer warp 0, lane 0)
+    const WsRing R{reinterpret_cast<WsRound*>(ws_smem), full, empty};
+    const StepArgs& a = g.base;
+    const StepParams P = params_of(a.k);
+    const unsigned t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const uint64_t npairs = a.n >> 1;
+    const unsigned ngroups = (unsigned)((npairs + 31) / 32);
+#if FSB_WGRID_STRIPED
+    // the CTA's stripes b, b + grid, ... (as step_kernel_ws): one moving front
+    const unsigned nstripes = (ngroups + kWsConsumers - 1) / kWsConsumers;
+    const unsigned rounds = nstripes > blockIdx.x ? (nstripes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+    const unsigned glo = blockIdx.x * kWsConsumers, gstride = gridDim.x * kWsConsumers;
+    const uint64_t limit = npairs;
+#else
+    // one balanced contiguous chunk
+    const unsigned glo = (unsigned)((uint64_t)ngroups * blockIdx.x / gridDim.x);
+    const unsigned ghi = (unsigned)((uint64_t)ngroups * (blockIdx.x + 1) / gridDim.x);
+    const uint64_t limit = ((uint64_t)ghi * 32 < npairs) ? (uint64_t)ghi * 32 : npairs;  // this chunk's pairs end
+    const unsigned rounds = (ghi - glo + kWsConsumers - 1) / kWsConsumers;
+    const unsigned gstride = kWsConsumers;
+#endif
+    if (t == 0) {
+        for (unsigned s = 0; s < kWsRounds; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kWsConsumers);
+        }
+        mbar_init(&stepdone, kWsConsumers);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        ecl = 0;
+    }
+    if (g.eclk && blockIdx.x == 0 && t == 32) {
+        g.eclk->g0 = gtimer();
+        g.eclk->c0 = clock64();
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            unsigned b = 0, ph = 0, issued = 0;
+            for (uint64_t k = 0; k < g.num_steps; ++k) {
+                const bool rev = a.alternate && ((g.first_step + k) & 1ull);
+                // step k reads what this CTA's consumers stored in step k-1
+                if (k && rounds) mbar_wait(&stepdone, (unsigned)((k - 1) & 1));
+                for (unsigned r = 0; r < rounds; ++r, ++issued) {
+                    if (issued >= kWsRounds) mbar_wait(&empty[b], ph ^ 1u);
+                    const uint64_t q0 = (uint64_t)(glo + (rev ? rounds - 1 - r : r) * gstride) * 32;
+                    ws_load(a, R, b, q0, (limit - q0 < kWsPairs) ? (unsigned)(limit - q0) : kWsPairs);
+                    if (++b == kWsRounds) {
+                        b = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;  // the producer takes no part in the consumers' named barriers
+    }
+    const unsigned c = warp - 1;
+    const unsigned kCons = kWsConsumers * 32;
+    unsigned b = 0, ph = 0;
+    double prev_best = -INFINITY;  // no pending eat at the start of a run
+    WsPair f;
+    bool have = false;  // f holds round 0 of the current step (fetched across the exchange)
+    for (uint64_t k = 0; k < g.num_steps; ++k) {
+        const uint64_t step = g.first_step + k;
+        const bool rev = a.alternate && (step & 1ull);
+        const bool eat = prev_best > 0.0;
+        const SharedDivisor M = make_divisor(eat ? prev_best : 1.0);
+        FSB_CHECK(ws_fast<true>(eat, M));  // in-range state, one rank: the divisor is in range
+        Partial acc = identity();
+        wgrid_rounds(f, have, a, P, eat, M, step, R, b, ph, c, glo, gstride, rounds, rev, limit, acc);
+        have = false;
+        // this warp's stores of step k, then the producer may read them with the
+        // async proxy (TMA) in step k+1
+        if (!FSB_WGRID_NOPROXY) asm volatile("fence.proxy.async.global;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&stepdone);
+        acc = warp_reduce(acc);
+        if (lane == 0) warp_part[c] = acc;
+        named_bar_sync(1, kCons);
+        if (c == 0) {
+            Partial blk = lane < kWsConsumers ? warp_part[lane] : identity();
+            blk = warp_reduce(blk);
+            const unsigned long long t_done = clock64();
+#if FSB_WGRID_TIMING  // TEMP experiment: the CTA's done time (ns) rides in sf
+            const double tg_done = (double)(gtimer() & 0xFFFFFFFFFFFull);
+            blk.sf = tg_done;
+#endif
+            Partial* slots = g.parts + (k & 1) * gridDim.x;  // reused at k+2: every CTA read it before arriving at k+1
+            if (lane == 0) {
+                store_partial(&slots[blockIdx.x], blk);
+#if FSB_WGRID_RELAXED  // TEMP experiment (not a valid protocol): no release on the arrival
+                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(g.gen), "l"(1ull) : "memory");
+#else
+                red_add_release_gpu(g.gen, 1ull);
+#endif
+                spin_until_gpu(g.gen, (k + 1) * (unsigned long long)gridDim.x);
+            }
+            __syncwarp();
+            Partial v[kWGridMaxGrid / 32];
+#pragma unroll
+            for (unsigned i = 0; i < kWGridMaxGrid / 32; ++i) {
+                const unsigned j = lane + 32 * i;
+                v[i] = j < gridDim.x ? load_cg(&slots[j]) : identity();
+            }
+            Partial tot = identity();
+#pragma unroll
+            for (unsigned i = 0; i < kWGridMaxGrid / 32; ++i) fold(tot, v[i]);
+            tot = warp_reduce(tot);
+#if FSB_WGRID_TIMING
+            double tmax = 0.0, tmin = 1e300;
+#pragma unroll
+            for (unsigned i = 0; i < kWGridMaxGrid / 32; ++i) {
+                if (lane + 32 * i < gridDim.x) {
+                    tmax = fmax(tmax, v[i].sf);
+                    tmin = fmin(tmin, v[i].sf);
+                }
+            }
+            for (int o = 16; o; o >>= 1) {
+                tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+                tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
+            }
+            const double tg_have = (double)(gtimer() & 0xFFFFFFFFFFFull);
+            if (lane == 0 && blockIdx.x == 0 && g.bary) {
+                g.bary[3 * k + 0] = tg_done - tmin;     // this CTA (0) done after the first CTA
+                g.bary[3 * k + 1] = tmax - tmin;        // spread of the CTAs' done times
+                g.bary[3 * k + 2] = tg_have - tmax;     // last CTA done -> total held by CTA 0
+            }
+            tot.sx = tot.sy = tot.sf = 0.0;
+#endif
+            if (lane == 0) {
+                shared_tot = tot;
+                ecl += clock64() - t_done;
+                if (blockIdx.x == 0) {
+                    g.trace[k] = tot.best;
+                    if (g.bary && !FSB_WGRID_TIMING) {
+                        g.bary[3 * k + 0] = tot.sx;
+                        g.bary[3 * k + 1] = tot.sy;
+                        g.bary[3 * k + 2] = tot.sf;
+                    }
+                    if (k + 1 == g.num_steps) store_partial(g.part_out, tot);
+                }
+            }
+        }
+        // the next step's first round needs no max: draw and fetch it now
+        if (k + 1 < g.num_steps && rounds) {
+            const uint64_t nstep = step + 1;
+            const bool nrev = a.alternate && (nstep & 1ull);
+            ws_fetch(f, a, P, nstep, R, b, ph, c, glo + (nrev ? rounds - 1 : 0u) * gstride, limit);
+            have = true;
+        }
+        named_bar_sync(2, kCons);
+        prev_best = shared_tot.best;
+    }
+    if (c == 0 && lane == 0 && g.eclk) {
+        atomicAdd(&g.eclk->ns, (unsigned long long)ecl);
+        if (blockIdx.x == 0) {
+            g.eclk->g1 = gtimer();
+            g.eclk->c1 = clock64();
+        }
+    }
 }
 
 
@@ -1764,6 +2271,23 @@ int step_dyn_blocks(int device) {
     return num_sms(device) * (per_sm < 1 ? 1 : per_sm);
 }
 
+int step_ws_blocks(int device) {
+    bool ok = true;
+    for (auto k : {step_kernel_ws<false>, step_kernel_ws<true>}) {
+        int per_sm = 0;
+        ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmemBytes) ==
+                       cudaSuccess;
+        ok = ok && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWsThreads, kWsSmemBytes) ==
+                       cudaSuccess &&
+             per_sm >= 1;
+    }
+    if (!ok) {
+        cudaGetLastError();
+        return 0;
+    }
+    return num_sms(device);  // one CTA per SM: the ring is sized for the SM's shared memory
+}
+
 int step_grid_blocks(int device, bool explicit_cur, bool bulk) {
     int per_sm = 0;
     cudaError_t e;
@@ -1812,6 +2336,9 @@ cudaError_t launch_maybe_pdl(void (*kern)(Args), int grid, int block, size_t sme
 cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
     const bool pdl = a.pdl != 0;
     const bool sane = a.sane != 0;
+    if (a.wspec && !a.s.c)
+        return launch_maybe_pdl(sane ? step_kernel_ws<true> : step_kernel_ws<false>, grid, kWsThreads, kWsSmemBytes,
+                                st, a, pdl);
     if (a.dyn && !a.bulk) {
         if (a.s.c)
             return launch_maybe_pdl(sane ? step_kernel_dyn<true, true> : step_kernel_dyn<true, false>, grid,
@@ -1827,6 +2354,31 @@ cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
                                 kBulkSmemBytes, st, a, pdl);
     return launch_maybe_pdl(sane ? step_kernel<false, true> : step_kernel<false, false>, grid, kStepThreads, 0, st, a,
                             pdl);
+}
+
+int wgrid_blocks(int device) {
+    if (num_sms(device) > (int)kWGridMaxGrid) return 0;
+    bool ok = true;
+    {
+        auto k = wgrid_kernel;
+        int per_sm = 0;
+        ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmemBytes) ==
+                       cudaSuccess;
+        ok = ok && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWsThreads, kWsSmemBytes) ==
+                       cudaSuccess &&
+             per_sm >= 1;
+    }
+    if (!ok) {
+        cudaGetLastError();
+        return 0;
+    }
+    return num_sms(device);
+}
+
+cudaError_t launch_wgrid_run(const WGridArgs& g, int grid, cudaStream_t st) {
+    void* args[] = {const_cast<WGridArgs*>(&g)};
+    if (!g.base.sane || g.base.world != 1) return cudaErrorInvalidValue;  // in-range state, one rank only
+    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(wgrid_kernel), dim3(grid), dim3(kWsThreads), args, kWsSmemBytes, st);
 }
 
 cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st) {

@@ -81,6 +81,18 @@ VARIANTS = {
     "dg1": ["-DFSB_DYN_MIN_GROUPS=1"],
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
+    # warp-specialised kernel: round buffers in the ring; memory-only / no-load / compute-only probes
+    "wsr2": ["-DFSB_WS_ROUNDS=2"],
+    "ws640u2": ["-DFSB_WS_THREADS=640", "-DFSB_WS_U=2", "-DFSB_WS_ROUNDS=2"],
+    "ws640u2c": ["-DFSB_WS_THREADS=640", "-DFSB_WS_U=2", "-DFSB_WS_ROUNDS=2", "-DFSB_WS_EXP=3"],
+    "wgchunk": ["-DFSB_WGRID_STRIPED=0"],
+    "wgtime": ["-DFSB_WGRID_TIMING=1"],
+    "wgtimechunk": ["-DFSB_WGRID_TIMING=1", "-DFSB_WGRID_STRIPED=0"],
+    "wgtimerelax": ["-DFSB_WGRID_TIMING=1", "-DFSB_WGRID_RELAXED=1"],
+    "wgtimenoproxy": ["-DFSB_WGRID_TIMING=1", "-DFSB_WGRID_NOPROXY=1"],
+    "wsmem": ["-DFSB_WS_EXP=1"],
+    "wsnoload": ["-DFSB_WS_EXP=2"],
+    "wscompute": ["-DFSB_WS_EXP=3"],
 }
 
 
