@@ -112,10 +112,6 @@ enum fsb_strategy {
 #define FSB_FLAG_WS_TILES 0x1000u   /* compact step kernel warp-specialised: per SM one producer warp streams
                                       the state HBM -> shared memory with cp.async.bulk through a deep
                                       mbarrier ring, 31 consumer warps compute from it and store to HBM */
-#define FSB_FLAG_WS_GRID 0x2000u    /* single-rank runs of in-range schools: all steps in one cooperative
-                                      launch of the warp-specialised kernel (per SM one producer warp and 31
-                                      consumer warps; a grid-wide exchange per step instead of a kernel
-                                      boundary); other runs are unaffected */
 #define FSB_FLAG_CHECKED 0x40u     /* always evaluate the fp64 fast-path operand guards (default: elided
                                       while config and state are provably in range; results identical) */
 

@@ -168,7 +168,6 @@ struct fsb_engine {
     bool use_bulk = false;   // compact step streams through the cp.async.bulk ring
     unsigned sg_cap = 0;     // shared-memory-resident grid: fish pairs per CTA (0: unavailable)
     int sg_grid = 0;         // ... its CTAs (one per SM)
-    int wg_grid = 0;         // CTAs of the warp-specialised persistent grid kernel (0: unavailable)
     unsigned long long* d_sg_keys = nullptr;  // [3] per-step max keys of the shared-memory grid
 
     void* staging = nullptr;  // device AoS staging (two halves of kStagingFish / 2 fish: double-buffered transfers)
@@ -615,60 +614,6 @@ int run_grid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, doub
     return FSB_OK;
 }
 
-// FSB_FLAG_WS_GRID: all T steps in one cooperative launch of the
-// warp-specialised persistent kernel (one 1024-thread CTA per SM, single rank,
-// in-range compact state), then the trailing eat kernel.
-bool want_wgrid(const fsb_engine* e) {
-    if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode || e->host_xchg || !in_range(e)) return false;
-    if (e->wg_grid <= 0 || e->count < 2 * 32 * (uint64_t)e->wg_grid) return false;
-    if (e->strategy == FSB_STRATEGY_STREAM || e->strategy == FSB_STRATEGY_PERSISTENT) return false;
-    return (e->flags & FSB_FLAG_WS_GRID) != 0;
-}
-
-int run_wgrid(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary, double* seconds) {
-    FSB_NVTX("run_wgrid: warp-specialised persistent grid kernel");
-    TRY(ensure_run_buffers(e, T));
-    fsb_dev::WGridArgs g{};
-    g.base = step_args(e, canonical(e));
-    g.first_step = first_step;
-    g.num_steps = T;
-    g.trace = e->d_cl_trace;
-    g.bary = bary ? e->d_cl_bary : nullptr;
-    g.gen = e->d_gen;
-    g.parts = e->block_part;  // block_cap >= 2 x grid_coop >= 2 x SMs
-    g.part_out = local_part(e, 0);
-    g.eclk = e->eclk;
-    CU(cudaMemsetAsync(e->eclk, 0, sizeof(fsb_dev::EatClock), e->stream));
-    CU(cudaMemsetAsync(e->d_gen, 0, sizeof(unsigned long long), e->stream));
-    CU(cudaEventRecord(e->ev0, e->stream));
-    cudaError_t ce = fault_injected("wgrid") ? cudaErrorCooperativeLaunchTooLarge
-                                             : fsb_dev::launch_wgrid_run(g, e->wg_grid, e->stream);
-    if (ce != cudaSuccess) {
-        cudaGetLastError();
-        const int code = co_schedule_refused(ce) ? FSB_ERR_UNSUPPORTED : FSB_ERR_CUDA;
-        return fail(code, std::string("ws grid: cooperative launch refused: ") + cudaGetErrorName(ce));
-    }
-    // the trailing eat of step T-1 (sim.hpp:115-121)
-    fsb_dev::EatArgs ea{};
-    ea.s = canonical(e);
-    ea.k = scalars_of(e->cfg);
-    ea.n = e->count;
-    ea.part_in = all_part(e, 0);
-    ea.world = 1;
-    CU(fsb_dev::launch_eat(ea, e->grid_aux, e->stream));
-    CU(cudaEventRecord(e->ev1, e->stream));
-    if (trace) CU(cudaMemcpyAsync(trace, e->d_cl_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
-    if (bary) CU(cudaMemcpyAsync(bary, e->d_cl_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
-    CU(cudaStreamSynchronize(e->stream));
-    TRY(elapsed(e, seconds));
-    TRY(read_eat_cycles(e, (double)e->wg_grid, &e->last_eat_s));
-    e->max_valid = e->sums_valid = true;
-    e->cur_buf = 0;
-    e->last_launches = 2;
-    e->last_strategy = FSB_STRATEGY_GRID;
-    return FSB_OK;
-}
-
 int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, double* bary,
                    double* seconds) {
     FSB_NVTX("run_persistent: persistent cluster kernel");
@@ -971,7 +916,6 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     e->block_cap = maxgrid;
     CB(cudaMalloc(&e->d_gen, sizeof(unsigned long long)));
     e->cgrid_nc = (e->flags & FSB_FLAG_FLAT_GRID) ? 0 : fsb_dev::cgrid_clusters(e->device);
-    if (e->world == 1) e->wg_grid = fsb_dev::wgrid_blocks(e->device);
     if (e->cgrid_nc > 0) {
         CB(cudaMalloc(&e->d_cl_slots, cl_slot_bytes(e)));
     }
@@ -1236,13 +1180,6 @@ int fsb_engine_run(fsb_engine* e, uint64_t first_step, uint64_t num_steps, doubl
         e->cur_buf = 0;
         e->last_launches = 0;
         e->last_strategy = FSB_STRATEGY_STREAM;
-    } else if (want_wgrid(e)) {
-        int rc = run_wgrid(e, first_step, num_steps, trace, bary, &secs);
-        if (rc == FSB_ERR_UNSUPPORTED && e->strategy == FSB_STRATEGY_AUTO) {
-            e->fallback = g_err;  // the device refused the co-resident grid: graph of step kernels
-            rc = run_stream_chunked(e, first_step, num_steps, trace, bary, &secs);
-        }
-        TRY(rc);
     } else if (want_grid(e)) {
         // (the first run after an inconsistent upload takes the stream path below)
         int rc = run_grid(e, first_step, num_steps, trace, bary, &secs);

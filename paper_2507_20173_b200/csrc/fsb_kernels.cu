@@ -1101,9 +1101,6 @@ __global__ void __launch_bounds__(kBulkThreads, FSB_BULK_MIN_BLOCKS) step_kernel
 #ifndef FSB_WS_ROUNDS
 #define FSB_WS_ROUNDS 3
 #endif
-#ifndef FSB_WS_EXP
-#define FSB_WS_EXP 0  // TEMP experiment: 1 memory only, 2 no loads, 3 no loads no stores
-#endif
 constexpr int kWsThreads = 1024;
 constexpr unsigned kWsConsumers = kWsThreads / 32 - 1;  // = groups per stripe
 constexpr unsigned kWsRounds = FSB_WS_ROUNDS;
@@ -1124,10 +1121,6 @@ struct WsRing {
 __device__ __forceinline__ void ws_load(const StepArgs& a, const WsRing& R, unsigned b, uint64_t q0, unsigned np) {
     const unsigned bytes = np * (unsigned)sizeof(double2);
     FSB_CHECK(np >= 1 && np <= kWsPairs);
-    if (FSB_WS_EXP >= 2) {
-        mbar_arrive(&R.full[b]);
-        return;
-    }
     mbar_expect_tx(&R.full[b], 4 * bytes);
     bulk_load(R.buf[b].x, reinterpret_cast<const double2*>(a.s.x) + q0, bytes, &R.full[b]);
     bulk_load(R.buf[b].y, reinterpret_cast<const double2*>(a.s.y) + q0, bytes, &R.full[b]);
@@ -1176,8 +1169,7 @@ __device__ __forceinline__ void ws_compute(WsPair& f, const StepArgs& a, const S
     double2* Y2 = reinterpret_cast<double2*>(a.s.y);
     double2* W2 = reinterpret_cast<double2*>(a.s.w);
     double2* P2 = reinterpret_cast<double2*>(a.s.p);
-    if (FSB_WS_EXP == 1) {
-    } else if (kFast) {
+    if (kFast) {
         if (f.valid[0]) {
             const double n0 = fish_sane(f.X[0].x, f.Y[0].x, f.W[0].x, f.Q[0].x, eat, M, f.dr.U0[0][0],
                                         f.dr.U1[0][0], P);
@@ -1191,7 +1183,7 @@ __device__ __forceinline__ void ws_compute(WsPair& f, const StepArgs& a, const S
         fused_pairs<false, 1, kSane, false, false, true>(f.X, f.Y, f.W, f.Q, f.X, f.valid, src, f.q, f.gi, P, eat, M,
                                                          step, acc, nullptr, &f.dr);
     }
-    if (f.valid[0] && FSB_WS_EXP != 3) {
+    if (f.valid[0]) {
         const uint64_t q = f.q[0];
         X2[q] = f.X[0];
         Y2[q] = f.Y[0];
@@ -1308,245 +1300,6 @@ __global__ void __launch_bounds__(kWsThreads, 1) step_kernel_ws(const StepArgs a
     }
     grid_publish(cta, a.ws, a.part_out, a.px, a.world, a.ec.out, t_done);
 }
-
-// ---------------------------------------------------------------------------
-// wgrid_kernel: all T steps of a single-rank school in ONE cooperative launch
-// of step_kernel_ws's warp specialisation (FSB_FLAG_WS_GRID).  Each CTA owns
-// one balanced contiguous chunk of 32-pair groups for the whole run, walked in
-// rounds of 31 groups (forwards on even steps, backwards on odd ones, so a
-// step's first rounds are the previous step's last, still in L2).  What the
-// persistent form removes from every step is the kernel boundary: the next
-// step's loads need only THIS CTA's stores of the previous step (the chunk is
-// its own), so the producer streams on as soon as the consumers have stored
-// and fenced their last round (a step-done mbarrier), while the consumers'
-// global max crosses the grid; the consumers meanwhile draw and fetch their
-// first round of the next step and only its arithmetic waits for the max.
-// Per step, consumer warp 0's lane 0 publishes the CTA partial (slot of step
-// parity), arrives on a grid counter and spins; the warp then folds all CTA
-// partials in index order (every CTA the same tree: bit-identical totals).
-// The explicit-cur state and multi-rank runs take the graph of step kernels;
-// the trailing eat is the engine's eat_kernel.
-
-#ifndef FSB_WGRID_STRIPED
-#define FSB_WGRID_STRIPED 1
-#endif
-#ifndef FSB_WGRID_TIMING
-#define FSB_WGRID_TIMING 0
-#endif
-#ifndef FSB_WGRID_RELAXED
-#define FSB_WGRID_RELAXED 0
-#endif
-#ifndef FSB_WGRID_NOPROXY
-#define FSB_WGRID_NOPROXY 0
-#endif
-constexpr unsigned kWGridMaxGrid = 160;  // consumer warp 0 folds <= 5 CTA partials per lane
-
-__device__ __forceinline__ void named_bar_sync(unsigned id, unsigned count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// One step of wgrid_kernel for consumer warp c: its group of every round of
-// the CTA's chunk (round 0 possibly fetched already), plus the school's odd
-// last fish (CTA 0, consumer warp 0, lane 0), all on the unguarded fast paths.
-__device__ __forceinline__ void wgrid_rounds(WsPair& f, bool have, const StepArgs& a, const StepParams& P, bool eat,
-                                             const SharedDivisor& M, uint64_t step, const WsRing& R, unsigned& b,
-                                             unsigned& ph, unsigned c, unsigned glo, unsigned gstride,
-                                             unsigned rounds, bool rev, uint64_t limit, Partial& acc) {
-    // stripe of round r: glo + r x gstride forwards, glo + (rounds - 1 - r) x gstride backwards
-    unsigned g = glo + (rev ? rounds - 1 : 0u) * gstride;
-    const unsigned d = rev ? 0u - gstride : gstride;
-    for (unsigned r = 0; r < rounds; ++r) {
-        if (r || !have) ws_fetch(f, a, P, step, R, b, ph, c, g, limit);
-        ws_compute<true, true>(f, a, P, eat, M, step, acc);
-        g += d;
-        if (++b == kWsRounds) {
-            b = 0;
-            ph ^= 1u;
-        }
-    }
-    if ((a.n & 1ull) && blockIdx.x == 0 && c == 0 && (threadIdx.x & 31) == 0) {  // the odd last fish (global)
-        const uint64_t i = a.n - 1;
-        double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];
-        const uint64_t h = fold_in(fold_in(P.seed, a.gfirst + i), step);
-        const double cn = fish_sane(x, y, w, p, eat, M, __ull2double_rn(fold_in(h, 0) >> 11),
-                                    __ull2double_rn(fold_in(h, 1) >> 11), P);
-        accumulate(acc, x, y, p, cn);
-        a.s.x[i] = x;
-        a.s.y[i] = y;
-        a.s.w[i] = w;
-        a.s.p[i] = p;
-    }
-}
-
-__global__ void __launch_bounds__(kWsThreads, 1) wgrid_kernel(const WGridArgs g) {
-    extern __shared__ __align__(128) unsigned char ws_smem[];
-    __shared__ __align__(8) uint64_t full[kWsRounds];
-    __shared__ __align__(8) uint64_t empty[kWsRounds];
-    __shared__ __align__(8) uint64_t stepdone;
-    __shared__ Partial warp_part[32];
-    __shared__ Partial shared_tot;
-    __shared__ unsigned long long ecl;  // eat-region SM cycles (consumer warp 0, lane 0)
-    const WsRing R{reinterpret_cast<WsRound*>(ws_smem), full, empty};
-    const StepArgs& a = g.base;
-    const StepParams P = params_of(a.k);
-    const unsigned t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const uint64_t npairs = a.n >> 1;
-    const unsigned ngroups = (unsigned)((npairs + 31) / 32);
-#if FSB_WGRID_STRIPED
-    // the CTA's stripes b, b + grid, ... (as step_kernel_ws): one moving front
-    const unsigned nstripes = (ngroups + kWsConsumers - 1) / kWsConsumers;
-    const unsigned rounds = nstripes > blockIdx.x ? (nstripes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-    const unsigned glo = blockIdx.x * kWsConsumers, gstride = gridDim.x * kWsConsumers;
-    const uint64_t limit = npairs;
-#else
-    // one balanced contiguous chunk
-    const unsigned glo = (unsigned)((uint64_t)ngroups * blockIdx.x / gridDim.x);
-    const unsigned ghi = (unsigned)((uint64_t)ngroups * (blockIdx.x + 1) / gridDim.x);
-    const uint64_t limit = ((uint64_t)ghi * 32 < npairs) ? (uint64_t)ghi * 32 : npairs;  // this chunk's pairs end
-    const unsigned rounds = (ghi - glo + kWsConsumers - 1) / kWsConsumers;
-    const unsigned gstride = kWsConsumers;
-#endif
-    if (t == 0) {
-        for (unsigned s = 0; s < kWsRounds; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kWsConsumers);
-        }
-        mbar_init(&stepdone, kWsConsumers);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        ecl = 0;
-    }
-    if (g.eclk && blockIdx.x == 0 && t == 32) {
-        g.eclk->g0 = gtimer();
-        g.eclk->c0 = clock64();
-    }
-    __syncthreads();
-
-    if (warp == 0) {
-        if (lane == 0) {
-            unsigned b = 0, ph = 0, issued = 0;
-            for (uint64_t k = 0; k < g.num_steps; ++k) {
-                const bool rev = a.alternate && ((g.first_step + k) & 1ull);
-                // step k reads what this CTA's consumers stored in step k-1
-                if (k && rounds) mbar_wait(&stepdone, (unsigned)((k - 1) & 1));
-                for (unsigned r = 0; r < rounds; ++r, ++issued) {
-                    if (issued >= kWsRounds) mbar_wait(&empty[b], ph ^ 1u);
-                    const uint64_t q0 = (uint64_t)(glo + (rev ? rounds - 1 - r : r) * gstride) * 32;
-                    ws_load(a, R, b, q0, (limit - q0 < kWsPairs) ? (unsigned)(limit - q0) : kWsPairs);
-                    if (++b == kWsRounds) {
-                        b = 0;
-                        ph ^= 1u;
-                    }
-                }
-            }
-        }
-        return;  // the producer takes no part in the consumers' named barriers
-    }
-    const unsigned c = warp - 1;
-    const unsigned kCons = kWsConsumers * 32;
-    unsigned b = 0, ph = 0;
-    double prev_best = -INFINITY;  // no pending eat at the start of a run
-    WsPair f;
-    bool have = false;  // f holds round 0 of the current step (fetched across the exchange)
-    for (uint64_t k = 0; k < g.num_steps; ++k) {
-        const uint64_t step = g.first_step + k;
-        const bool rev = a.alternate && (step & 1ull);
-        const bool eat = prev_best > 0.0;
-        const SharedDivisor M = make_divisor(eat ? prev_best : 1.0);
-        FSB_CHECK(ws_fast<true>(eat, M));  // in-range state, one rank: the divisor is in range
-        Partial acc = identity();
-        wgrid_rounds(f, have, a, P, eat, M, step, R, b, ph, c, glo, gstride, rounds, rev, limit, acc);
-        have = false;
-        // this warp's stores of step k, then the producer may read them with the
-        // async proxy (TMA) in step k+1
-        if (!FSB_WGRID_NOPROXY) asm volatile("fence.proxy.async.global;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&stepdone);
-        acc = warp_reduce(acc);
-        if (lane == 0) warp_part[c] = acc;
-        named_bar_sync(1, kCons);
-        if (c == 0) {
-            Partial blk = lane < kWsConsumers ? warp_part[lane] : identity();
-            blk = warp_reduce(blk);
-            const unsigned long long t_done = clock64();
-#if FSB_WGRID_TIMING  // TEMP experiment: the CTA's done time (ns) rides in sf
-            const double tg_done = (double)(gtimer() & 0xFFFFFFFFFFFull);
-            blk.sf = tg_done;
-#endif
-            Partial* slots = g.parts + (k & 1) * gridDim.x;  // reused at k+2: every CTA read it before arriving at k+1
-            if (lane == 0) {
-                store_partial(&slots[blockIdx.x], blk);
-#if FSB_WGRID_RELAXED  // TEMP experiment (not a valid protocol): no release on the arrival
-                asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(g.gen), "l"(1ull) : "memory");
-#else
-                red_add_release_gpu(g.gen, 1ull);
-#endif
-                spin_until_gpu(g.gen, (k + 1) * (unsigned long long)gridDim.x);
-            }
-            __syncwarp();
-            Partial v[kWGridMaxGrid / 32];
-#pragma unroll
-            for (unsigned i = 0; i < kWGridMaxGrid / 32; ++i) {
-                const unsigned j = lane + 32 * i;
-                v[i] = j < gridDim.x ? load_cg(&slots[j]) : identity();
-            }
-            Partial tot = identity();
-#pragma unroll
-            for (unsigned i = 0; i < kWGridMaxGrid / 32; ++i) fold(tot, v[i]);
-            tot = warp_reduce(tot);
-#if FSB_WGRID_TIMING
-            double tmax = 0.0, tmin = 1e300;
-#pragma unroll
-            for (unsigned i = 0; i < kWGridMaxGrid / 32; ++i) {
-                if (lane + 32 * i < gridDim.x) {
-                    tmax = fmax(tmax, v[i].sf);
-                    tmin = fmin(tmin, v[i].sf);
-                }
-            }
-            for (int o = 16; o; o >>= 1) {
-                tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-                tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, o));
-            }
-            const double tg_have = (double)(gtimer() & 0xFFFFFFFFFFFull);
-            if (lane == 0 && blockIdx.x == 0 && g.bary) {
-                g.bary[3 * k + 0] = tg_done - tmin;     // this CTA (0) done after the first CTA
-                g.bary[3 * k + 1] = tmax - tmin;        // spread of the CTAs' done times
-                g.bary[3 * k + 2] = tg_have - tmax;     // last CTA done -> total held by CTA 0
-            }
-            tot.sx = tot.sy = tot.sf = 0.0;
-#endif
-            if (lane == 0) {
-                shared_tot = tot;
-                ecl += clock64() - t_done;
-                if (blockIdx.x == 0) {
-                    g.trace[k] = tot.best;
-                    if (g.bary && !FSB_WGRID_TIMING) {
-                        g.bary[3 * k + 0] = tot.sx;
-                        g.bary[3 * k + 1] = tot.sy;
-                        g.bary[3 * k + 2] = tot.sf;
-                    }
-                    if (k + 1 == g.num_steps) store_partial(g.part_out, tot);
-                }
-            }
-        }
-        // the next step's first round needs no max: draw and fetch it now
-        if (k + 1 < g.num_steps && rounds) {
-            const uint64_t nstep = step + 1;
-            const bool nrev = a.alternate && (nstep & 1ull);
-            ws_fetch(f, a, P, nstep, R, b, ph, c, glo + (nrev ? rounds - 1 : 0u) * gstride, limit);
-            have = true;
-        }
-        named_bar_sync(2, kCons);
-        prev_best = shared_tot.best;
-    }
-    if (c == 0 && lane == 0 && g.eclk) {
-        atomicAdd(&g.eclk->ns, (unsigned long long)ecl);
-        if (blockIdx.x == 0) {
-            g.eclk->g1 = gtimer();
-            g.eclk->c1 = clock64();
-        }
-    }
-}
-
 
 template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
@@ -2354,31 +2107,6 @@ cudaError_t launch_step(const StepArgs& a, int grid, cudaStream_t st) {
                                 kBulkSmemBytes, st, a, pdl);
     return launch_maybe_pdl(sane ? step_kernel<false, true> : step_kernel<false, false>, grid, kStepThreads, 0, st, a,
                             pdl);
-}
-
-int wgrid_blocks(int device) {
-    if (num_sms(device) > (int)kWGridMaxGrid) return 0;
-    bool ok = true;
-    {
-        auto k = wgrid_kernel;
-        int per_sm = 0;
-        ok = ok && cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWsSmemBytes) ==
-                       cudaSuccess;
-        ok = ok && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWsThreads, kWsSmemBytes) ==
-                       cudaSuccess &&
-             per_sm >= 1;
-    }
-    if (!ok) {
-        cudaGetLastError();
-        return 0;
-    }
-    return num_sms(device);
-}
-
-cudaError_t launch_wgrid_run(const WGridArgs& g, int grid, cudaStream_t st) {
-    void* args[] = {const_cast<WGridArgs*>(&g)};
-    if (!g.base.sane || g.base.world != 1) return cudaErrorInvalidValue;  // in-range state, one rank only
-    return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(wgrid_kernel), dim3(grid), dim3(kWsThreads), args, kWsSmemBytes, st);
 }
 
 cudaError_t launch_eat(const EatArgs& a, int grid, cudaStream_t st) {

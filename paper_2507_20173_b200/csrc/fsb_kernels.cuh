@@ -265,20 +265,6 @@ struct SGridArgs {
     unsigned long long* keys;     // [3] per-step max keys (max-only runs), zero at launch
 };
 
-// Warp-specialised persistent run (FSB_FLAG_WS_GRID): single rank, all
-// num_steps steps in one cooperative launch of one 1024-thread CTA per SM.
-struct WGridArgs {
-    StepArgs base;                // state, scalars, n, gfirst, sane, alternate
-    uint64_t first_step;
-    uint64_t num_steps;
-    double* trace;                // [num_steps]
-    double* bary;                 // [3*num_steps] or nullptr
-    unsigned long long* gen;      // arrival counter, zero at launch
-    Partial* parts;               // [2][grid] CTA partials
-    Partial* part_out;            // the last step's total (the trailing eat's part_in)
-    EatClock* eclk;               // eat-region clock (nullptr: off)
-};
-
 struct EatArgs {
     SoA s;
     Scalars k;
@@ -349,9 +335,6 @@ cudaError_t launch_grid_run(const GridArgs& g, int grid, cudaStream_t st);
 // hold (0: not available) for a grid of `grid` CTAs (one per SM).
 unsigned sgrid_pair_capacity(int device, int* grid);
 cudaError_t launch_sgrid_run(const SGridArgs& g, int grid, cudaStream_t st);
-// Warp-specialised persistent run: its grid (one CTA per SM; 0: not available).
-int wgrid_blocks(int device);
-cudaError_t launch_wgrid_run(const WGridArgs& g, int grid, cudaStream_t st);
 
 // Cluster kernel: returns cudaErrorNotSupported when n does not fit.
 int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta);

@@ -765,72 +765,3 @@ def test_smem_grid_and_l2_grid_bit_exact(orc, n, t):
         assert got.tobytes() == want_fish.tobytes(), (n, l2)
         assert rel_ok(bary[-1], ref), (n, l2)
         assert 0.0 < tm.seconds_eat < tm.seconds_loop
-
-
-# ---- warp-specialised persistent grid (FSB_FLAG_WS_GRID) -----------------------
-
-@pytest.mark.parametrize("n,t", [(9472, 5), (100_003, 7), (1_000_000, 4), (3_000_001, 3), (4_999_998, 2)])
-@pytest.mark.parametrize("alternate", [True, False])
-def test_ws_grid_bit_exact(orc, n, t, alternate):
-    """All steps in one cooperative launch of the warp-specialised kernel (per
-    CTA one contiguous chunk, a grid-wide exchange per step, the next step's
-    first round fetched across it), then the trailing eat: state, trace and
-    barycentre against the oracle; odd and ragged sizes, both walk orders."""
-    cfg = fsb.baseline_config(n, t)
-    want_fish, want_trace = orc.simulate(ocfg(cfg))
-    with make(cfg, "auto", ws_grid=True, alternate=alternate) as eng:
-        trace, bary, timing = eng.simulate(barycentre=True)
-        assert eng.last_strategy()[0] == "grid"
-        assert eng.last_launches() == 2
-        assert 0.0 < timing.seconds_eat < timing.seconds_loop
-        got = eng.download()
-    assert got.tobytes() == want_fish.tobytes()
-    assert trace.tobytes() == want_trace.tobytes()
-    assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
-
-
-def test_ws_grid_split_runs_and_phases(orc):
-    """Split runs (the walk order follows the global step parity), the phase API
-    after a ws-grid run (eat() of the run's last partial, move/eat), and a run
-    after an inconsistent upload (explicit-cur: the graph of step kernels)."""
-    n = 1_000_003
-    cfg = fsb.baseline_config(n, 9)
-    oc = ocfg(cfg)
-    fish = orc.init(oc)
-    with make(cfg, "auto", ws_grid=True) as eng:
-        eng.init()
-        for first, cnt in ((0, 3), (3, 1), (4, 2)):
-            trace, _, _ = eng.run(first, cnt)
-            assert trace.tobytes() == orc.run(oc, fish, first, cnt).tobytes()
-            assert eng.last_strategy()[0] == "grid"
-        assert eng.download().tobytes() == fish.tobytes()
-        eng.move(6)
-        orc.move(oc, 6, fish)
-        assert bits(eng.eat().max_diff) == bits(orc.eat(oc, fish))
-        school = eng.download()
-        school["current_objective"][::5] += 0.5
-        eng.upload(school)
-        want = school.copy()
-        trace, _, _ = eng.run(7, 2)
-        assert eng.last_strategy()[0] == "stream"  # explicit current_objective: graph of step kernels
-        assert trace.tobytes() == orc.run(oc, want, 7, 2).tobytes()
-        assert eng.download().tobytes() == want.tobytes()
-
-
-def test_ws_grid_repeatable_and_out_of_range_fallback(orc):
-    """Bitwise repeatable sums; an out-of-range (checked) state and explicit
-    strategies do not take the ws grid."""
-    cfg = fsb.baseline_config(500_001, 6)
-    outs = []
-    for _ in range(2):
-        with make(cfg, "auto", ws_grid=True) as eng:
-            trace, bary, _ = eng.simulate(barycentre=True)
-            outs.append((trace.tobytes(), bary.tobytes(), eng.checksum()))
-    assert outs[0] == outs[1]
-    want_fish, want_trace = orc.simulate(ocfg(cfg))
-    for kw in (dict(checked=True), dict(strategy="stream")):
-        with make(cfg, **{"strategy": "auto", "ws_grid": True, **kw}) as eng:
-            trace, _, _ = eng.simulate()
-            assert eng.last_launches() != 2  # not the ws grid (AUTO: the grid kernels up to 2.5e6 fish)
-            assert trace.tobytes() == want_trace.tobytes()
-            assert eng.download().tobytes() == want_fish.tobytes()

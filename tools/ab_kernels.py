@@ -20,7 +20,6 @@ KERNELS = {
     "flatgrid": dict(strategy="grid", flat_grid=True),
     "bulk": dict(bulk=True),          # cp.async.bulk shared-memory ring
     "ws": dict(ws_tiles=True),        # warp-specialised: TMA producer warp + 31 consumer warps
-    "wsgrid": dict(strategy="auto", ws_grid=True),  # the same, all steps in one cooperative launch
 }
 names = (sys.argv[1] if len(sys.argv) > 1 else "dyn,static,bulk").split(",")
 sizes = [(1_000_000, 100), (10_000_000, 100), (100_000_000, 20)]

@@ -21,6 +21,12 @@ profiles/r04_ab_session.jsonl), the register double-buffered claimed-tile
 kernel (FSB_DYN_PIPE, profiles/r05_ab_pipe.jsonl) and the contiguous-chunk
 claimed tiles (FSB_DYN_STRIPED=0).  Their sources are in git history at
 commit 7dc3518 (`git show 7dc3518:paper_2507_20173_b200/csrc/fsb_kernels.cu`).
+Round 2, session 3, removed after measurement (sources at commit 3ae1e18):
+the warp-specialised kernel's memory-only / no-load / compute-only probes
+(FSB_WS_EXP), its 640-thread two-groups-per-consumer form (FSB_WS_U), and the
+persistent warp-specialised grid (FSB_FLAG_WS_GRID, wgrid_kernel) with its
+per-step timing build -- profiles/round2_ab_ws_variants.jsonl,
+profiles/round2_ab_wsgrid.jsonl, profiles/round2_wgrid_timing.txt.
 """
 from __future__ import annotations
 
@@ -81,18 +87,8 @@ VARIANTS = {
     "dg1": ["-DFSB_DYN_MIN_GROUPS=1"],
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
-    # warp-specialised kernel: round buffers in the ring; memory-only / no-load / compute-only probes
+    # warp-specialised kernel (FSB_FLAG_WS_TILES): round buffers in the ring
     "wsr2": ["-DFSB_WS_ROUNDS=2"],
-    "ws640u2": ["-DFSB_WS_THREADS=640", "-DFSB_WS_U=2", "-DFSB_WS_ROUNDS=2"],
-    "ws640u2c": ["-DFSB_WS_THREADS=640", "-DFSB_WS_U=2", "-DFSB_WS_ROUNDS=2", "-DFSB_WS_EXP=3"],
-    "wgchunk": ["-DFSB_WGRID_STRIPED=0"],
-    "wgtime": ["-DFSB_WGRID_TIMING=1"],
-    "wgtimechunk": ["-DFSB_WGRID_TIMING=1", "-DFSB_WGRID_STRIPED=0"],
-    "wgtimerelax": ["-DFSB_WGRID_TIMING=1", "-DFSB_WGRID_RELAXED=1"],
-    "wgtimenoproxy": ["-DFSB_WGRID_TIMING=1", "-DFSB_WGRID_NOPROXY=1"],
-    "wsmem": ["-DFSB_WS_EXP=1"],
-    "wsnoload": ["-DFSB_WS_EXP=2"],
-    "wscompute": ["-DFSB_WS_EXP=3"],
 }
 
 
