@@ -637,6 +637,7 @@ int run_persistent(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace
     a.bary = bary ? e->d_cl_bary : nullptr;  // max-only reduction unless sums are wanted
     a.part_out = local_part(e, 0);
     a.eclk = std::getenv("FSB_NO_EAT_CLOCK") ? nullptr : e->eclk;  // (A/B of the clock's cost)
+    a.sane = in_range(e) ? 1 : 0;
     CU(cudaMemsetAsync(e->eclk, 0, sizeof(fsb_dev::EatClock), e->stream));
     CU(cudaEventRecord(e->ev0, e->stream));
     int ctas = 0;

@@ -1441,7 +1441,17 @@ __device__ __forceinline__ void st_async_f64(uint32_t dst, double a, uint32_t ba
                  : "memory");
 }
 
+// Wait for a phase of this CTA's mbarrier whose bytes other CTAs of the
+// cluster deliver with st.async (complete_tx): the data and the barrier are
+// both in this CTA's shared memory, so the default CTA-scope acquire orders
+// the reads of the delivered slots.  A cluster-scope acquire would also
+// invalidate L1 on every wait (CCTL.IVALL: 20% of the C4 step's stall samples,
+// profiles/round2_cluster_kernel_c4_ncu_source_top.txt).
+#ifndef FSB_CLUSTER_ACQ
+#define FSB_CLUSTER_ACQ 0  // A/B: 1 = acquire at cluster scope
+#endif
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity) {
+#if FSB_CLUSTER_ACQ
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "FSB_CWAIT_%=:\n\t"
@@ -1449,11 +1459,23 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, unsigned parity
         "@!p bra FSB_CWAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "FSB_CWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra FSB_CWAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#endif
 }
 
 // kBary: also reduce the barycentre sums each step (only when the caller asked
 // for them -- the max alone is a 4x shorter reduction on this latency-bound path).
-template <int F, bool kBary, bool kClock>
+// kSane: in-range state (init'd or checked at upload): every division and
+// square root on its unguarded fast path (fish_sane_cur) -- one rank, so the
+// divisor (the school's own max) is in range too.
+template <int F, bool kBary, bool kClock, bool kSane>
 __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     cg::cluster_group cluster = cg::this_cluster();
     const unsigned crank = cluster.block_rank();
@@ -1500,7 +1522,10 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     if (kClock) eclk_bracket(a.eclk, false);
     double u0[F], u1[F];  // this step's RNG draws, made during the previous barrier
 #pragma unroll
-    for (int f = 0; f < F; ++f) draw_units(hf[f], a.first_step, u0[f], u1[f]);
+    for (int f = 0; f < F; ++f) {
+        if (kSane) draw_ints(hf[f], a.first_step, u0[f], u1[f]);
+        else draw_units(hf[f], a.first_step, u0[f], u1[f]);
+    }
     for (uint64_t k = 0; k < a.num_steps; ++k) {
         const uint64_t step = a.first_step + k;
         const unsigned b = (unsigned)(k & 1);
@@ -1512,9 +1537,14 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
 #pragma unroll
         for (int f = 0; f < F; ++f) {
             if (valid[f]) {
-                if (eat) w[f] = eat_weight(w[f], p[f], c[f], D, P.w_max);
-                const double cn = swim_with_units(x[f], y[f], w[f], u0[f], u1[f], P);
-                p[f] = c[f];
+                double cn;
+                if (kSane) {
+                    cn = fish_sane_cur(x[f], y[f], w[f], p[f], c[f], eat, D, u0[f], u1[f], P);
+                } else {
+                    if (eat) w[f] = eat_weight(w[f], p[f], c[f], D, P.w_max);
+                    cn = swim_with_units(x[f], y[f], w[f], u0[f], u1[f], P);
+                    p[f] = c[f];
+                }
                 c[f] = cn;
                 if (kBary) {
                     accumulate(acc, x[f], y[f], p[f], cn);
@@ -1540,7 +1570,10 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         }
         // draw the next step's random numbers while the partials travel
 #pragma unroll
-        for (int f = 0; f < F; ++f) draw_units(hf[f], step + 1, u0[f], u1[f]);
+        for (int f = 0; f < F; ++f) {
+            if (kSane) draw_ints(hf[f], step + 1, u0[f], u1[f]);
+            else draw_units(hf[f], step + 1, u0[f], u1[f]);
+        }
         mbar_wait_cluster(&xbar[b], (unsigned)((k >> 1) & 1));
         if (kClock && threadIdx.x == 0) ecl += clock64() - t_done;
         tot = identity();
@@ -2275,8 +2308,10 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
     (void)device;
     static int cached = 0;
     if (!cached) {
-        for (auto k : {cluster_kernel<kClusterF, true, true>, cluster_kernel<kClusterF, false, true>,
-                       cluster_kernel<kClusterF, true, false>, cluster_kernel<kClusterF, false, false>})
+        for (auto k : {cluster_kernel<kClusterF, true, true, false>, cluster_kernel<kClusterF, false, true, false>,
+                       cluster_kernel<kClusterF, true, false, false>, cluster_kernel<kClusterF, false, false, false>,
+                       cluster_kernel<kClusterF, true, true, true>, cluster_kernel<kClusterF, false, true, true>,
+                       cluster_kernel<kClusterF, true, false, true>, cluster_kernel<kClusterF, false, false, true>})
             cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         cached = 8;
         for (int c : {16, 8}) {
@@ -2291,7 +2326,8 @@ int cluster_capacity(int device, int* cluster_ctas, int* threads_per_cta) {
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             int nclusters = 0;
-            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<kClusterF, true, true>, &cfg) == cudaSuccess &&
+            if (cudaOccupancyMaxActiveClusters(&nclusters, cluster_kernel<kClusterF, true, true, false>, &cfg) ==
+                    cudaSuccess &&
                 nclusters >= 1) {
                 cached = c;
                 break;
@@ -2332,12 +2368,18 @@ cudaError_t launch_cluster_run(const ClusterArgs& a, cudaStream_t st, int* ctas)
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (ctas) *ctas = (int)ncta;
-    if (a.eclk) {
-        if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true, true>, a);
-        return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false, true>, a);
+#define FSB_CL_LAUNCH(S)                                                                   \
+    if (a.eclk) {                                                                          \
+        if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true, true, S>, a); \
+        return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false, true, S>, a);     \
+    }                                                                                      \
+    if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true, false, S>, a); \
+    return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false, false, S>, a);
+    if (a.sane) {
+        FSB_CL_LAUNCH(true)
     }
-    if (a.bary) return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, true, false>, a);
-    return cudaLaunchKernelEx(&cfg, cluster_kernel<kClusterF, false, false>, a);
+    FSB_CL_LAUNCH(false)
+#undef FSB_CL_LAUNCH
 }
 
 }  // namespace fsb_dev

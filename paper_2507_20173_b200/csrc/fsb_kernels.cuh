@@ -309,6 +309,7 @@ struct ClusterArgs {
     double* bary;         // [3*num_steps] or nullptr
     Partial* part_out;    // final step partial (for a later eat())
     EatClock* eclk;       // eat-region clock: per-CTA cycles summed in ns, brackets in g/c (nullptr: off)
+    int sane;             // in-range state: unguarded fast paths (fsb_math.cuh "In-range mode")
 };
 
 int step_grid_blocks(int device, bool explicit_cur, bool bulk);

@@ -80,6 +80,8 @@ def main():
         if a.checked_ab and n > 32768:
             for bulk in (True, False):
                 print(json.dumps(time_cfg(name, n, t, "stream", True, a.reps, bulk, checked=True)), flush=True)
+        if a.checked_ab and n <= 16384:  # the persistent kernel with its guarded (non-in-range) paths
+            print(json.dumps(time_cfg(name, n, t, "auto", True, a.reps, False, checked=True)), flush=True)
         if a.grid_ab and n > 16384:
             print(json.dumps(time_cfg(name, n, t, "grid", True, a.reps, False)), flush=True)
 

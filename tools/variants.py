@@ -26,7 +26,10 @@ the warp-specialised kernel's memory-only / no-load / compute-only probes
 (FSB_WS_EXP), its 640-thread two-groups-per-consumer form (FSB_WS_U), and the
 persistent warp-specialised grid (FSB_FLAG_WS_GRID, wgrid_kernel) with its
 per-step timing build -- profiles/round2_ab_ws_variants.jsonl,
-profiles/round2_ab_wsgrid.jsonl, profiles/round2_wgrid_timing.txt.
+profiles/round2_ab_wsgrid.jsonl, profiles/round2_wgrid_timing.txt; and the
+persistent cluster kernel's per-phase SM-cycle stamps (clock64 around the fish
+update, the block reduction and the DSMEM exchange of thread 0 of every CTA;
+method and numbers in profiles/round2_cluster_phases.txt).
 """
 from __future__ import annotations
 
@@ -65,6 +68,9 @@ VARIANTS = {
     "cg16": ["-DFSB_CGRID_CLUSTER=16"],
     # persistent cluster kernel: fish per CTA before another CTA is added
     "c512": ["-DFSB_CLUSTER_MIN_FISH=512"],
+    "c128": ["-DFSB_CLUSTER_MIN_FISH=128"],
+    # persistent cluster / cluster-grid kernels: acquire at cluster scope on the DSMEM mbarrier waits
+    "clacq": ["-DFSB_CLUSTER_ACQ=1"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
     # persistent cluster kernel: fish per thread
     "cf2": ["-DFSB_CLUSTER_F=2"],
