@@ -1834,6 +1834,10 @@ constexpr int kSGridU = FSB_SGRID_U;          // pairs per pass (independent cha
 #define FSB_SGRID_PRE 1
 #endif
 constexpr bool kSGridPre = FSB_SGRID_PRE;     // keep fold_in(seed, fish) of the thread's pairs in registers
+#ifndef FSB_SGRID_PREDRAW
+#define FSB_SGRID_PREDRAW 1
+#endif
+constexpr bool kSGridPreDraw = FSB_SGRID_PREDRAW;  // draw the first pair's next-step RNG during the barrier
 
 template <bool kSane, bool kBary>
 __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs g) {
@@ -1890,6 +1894,15 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
 
     const SoA2 src{sx, sy, sw, sp, nullptr};
     double prev_best = -INFINITY;  // no pending eat at the start of a run
+    // the next step's draws of the thread's first pair, made while the CTA waits
+    // at the step's grid barrier (in-range runs; the draws need no max)
+    double pre[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    auto predraw = [&](uint64_t nstep, bool more) {
+        if (kSane && kSGridPre && kSGridPreDraw && more && t < cnt) {
+            draw_ints(H[0][0], nstep, pre[0][0], pre[0][1]);
+            draw_ints(H[0][1], nstep, pre[1][0], pre[1][1]);
+        }
+    };
     for (uint64_t k = 0; k < g.num_steps; ++k) {
         const uint64_t step = g.first_step + k;
         const bool eat = prev_best > 0.0;
@@ -1913,8 +1926,32 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
                     W[u] = sw[qs[u]];
                     Q[u] = sp[qs[u]];
                 }
-                fused_pairs<false, kSGridU, kSane, false, kSGridPre>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M,
-                                                                     step, acc, &H[kSGridPre ? j : 0][0]);
+                if (kSane && kSGridPre) {
+                    // one rank in range: the divisor (the school's own max) is in range too, so
+                    // nothing is guarded and there is no fallback call in the step loop
+#pragma unroll
+                    for (int u = 0; u < kSGridU; ++u) {
+                        if (valid[u]) {
+                            double m[2][2];
+                            if (kSGridPreDraw && j == 0 && u == 0 && k > 0) {  // drawn during the last barrier
+                                m[0][0] = pre[0][0];
+                                m[0][1] = pre[0][1];
+                                m[1][0] = pre[1][0];
+                                m[1][1] = pre[1][1];
+                            } else {
+                                draw_ints(H[kSGridPre ? j + u : 0][0], step, m[0][0], m[0][1]);
+                                draw_ints(H[kSGridPre ? j + u : 0][1], step, m[1][0], m[1][1]);
+                            }
+                            const double n0 = fish_sane(X[u].x, Y[u].x, W[u].x, Q[u].x, eat, M, m[0][0], m[0][1], P);
+                            const double n1 = fish_sane(X[u].y, Y[u].y, W[u].y, Q[u].y, eat, M, m[1][0], m[1][1], P);
+                            accumulate(acc, X[u].x, Y[u].x, Q[u].x, n0);
+                            accumulate(acc, X[u].y, Y[u].y, Q[u].y, n1);
+                        }
+                    }
+                } else {
+                    fused_pairs<false, kSGridU, kSane, false, kSGridPre>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M,
+                                                                         step, acc, &H[kSGridPre ? j : 0][0]);
+                }
 #pragma unroll
                 for (int u = 0; u < kSGridU; ++u) {
                     if (valid[u]) {
@@ -1941,8 +1978,9 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
             if (t == 0) {
                 store_partial(&slots[blockIdx.x], blk);
                 red_add_release_gpu(g.gen, 1ull);
-                spin_until_gpu(g.gen, target);
             }
+            predraw(step + 1, k + 1 < g.num_steps);
+            if (t == 0) spin_until_gpu(g.gen, target);
             __syncthreads();
             if (t < 32) {
                 Partial v[kSGridMaxGrid / 32];
@@ -1969,10 +2007,13 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
         } else {
             // max only: the key of the CTA max, one red.max per CTA into this step's key slot
             const unsigned long long key = block_max_key(max_key(acc.best), scratch_key, &t_done, true);
+            unsigned long long* slot = g.keys + k % 3;
             if (t == 0) {
-                unsigned long long* slot = g.keys + k % 3;
                 red_max_relaxed_gpu(slot, key);
                 red_add_release_gpu(g.gen, 1ull);  // orders the red.max before the arrival
+            }
+            predraw(step + 1, k + 1 < g.num_steps);
+            if (t == 0) {
                 spin_until_gpu(g.gen, target);
                 const double m = key_value(*reinterpret_cast<volatile unsigned long long*>(slot));
                 // slot (k+2)%3 was last read at step k-1 by every CTA (all arrived at k since):

@@ -87,6 +87,7 @@ VARIANTS = {
     "spinacq": ["-DFSB_SPIN_ACQ=1"],
     "sg512u2np": ["-DFSB_SGRID_U=2", "-DFSB_SGRID_PRE=0"],
     "sg512np": ["-DFSB_SGRID_PRE=0"],
+    "sgnopredraw": ["-DFSB_SGRID_PREDRAW=0"],
     "sg1024np": ["-DFSB_SGRID_THREADS=1024", "-DFSB_SGRID_PAIRS=4", "-DFSB_SGRID_PRE=0"],
     "sg768u2np": ["-DFSB_SGRID_THREADS=768", "-DFSB_SGRID_PAIRS=5", "-DFSB_SGRID_U=2", "-DFSB_SGRID_PRE=0"],
     # claimed-tile kernel: minimum 32-pair groups per tile
