@@ -459,7 +459,11 @@ __device__ __forceinline__ void draw_pairs(PairDraws<U>& d, const uint64_t (&gi)
 
 // kDrawn: DR holds the pairs' draws, made by the caller ahead of the state
 // (step_kernel_ws draws before it waits for the stage to land).
-template <bool kExplicitCur, int U, bool kSane, bool kRngFirst = false, bool kPre = false, bool kDrawn = false>
+// kFast (with kSane and kRngFirst): the caller has checked the divisor's range
+// for the launch, so nothing is guarded -- sqrt_sane, unguarded divisions, no
+// vote and no fallback call in the caller's loop.
+template <bool kExplicitCur, int U, bool kSane, bool kRngFirst = false, bool kPre = false, bool kDrawn = false,
+          bool kFast = false>
 __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], double2 (&W)[U],
                                             double2 (&Q)[U], const double2 (&C)[U], const bool (&valid)[U],
                                             const SoA2& src, const uint64_t (&k)[U], const uint64_t (&gi)[U],
@@ -520,7 +524,15 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             ok[u] = ok0;
-            if (valid[u]) {
+            if (kFast && valid[u]) {
+                const double c0 = kExplicitCur ? C[u].x : objective_sane(X[u].x, Y[u].x, hp);
+                const double c1 = kExplicitCur ? C[u].y : objective_sane(X[u].y, Y[u].y, hp);
+                double w0 = fenced(W[u].x), w1 = fenced(W[u].y), p0 = Q[u].x, p1 = Q[u].y;
+                n0[u] = fish_sane_cur(X[u].x, Y[u].x, w0, p0, c0, eat, M, U0[u][0], U1[u][0], P);
+                n1[u] = fish_sane_cur(X[u].y, Y[u].y, w1, p1, c1, eat, M, U0[u][1], U1[u][1], P);
+                W[u] = make_double2(w0, w1);
+                Q[u] = make_double2(p0, p1);
+            } else if (valid[u]) {
                 const double c0 = kExplicitCur ? C[u].x : objective_guarded<kSane>(X[u].x, Y[u].x, hp, ok[u]);
                 const double c1 = kExplicitCur ? C[u].y : objective_guarded<kSane>(X[u].y, Y[u].y, hp, ok[u]);
                 double w0 = fenced(W[u].x);
@@ -550,7 +562,7 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
             }
         }
     }
-    if (__any_sync(__activemask(), !all_ok)) {  // never taken for in-range simulation values
+    if (!kFast && __any_sync(__activemask(), !all_ok)) {  // never taken for in-range simulation values
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (valid[u] && !ok[u]) {
@@ -576,6 +588,14 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
             accumulate(acc, X[u].y, Y[u].y, Q[u].y, n1[u]);
         }
     }
+}
+
+// In-range state and an in-range divisor (the global max, which other ranks'
+// states feed: checked once per step) leave nothing to guard.
+template <bool kSane>
+__device__ __forceinline__ bool no_guards(bool eat, const SharedDivisor& M) {
+    const uint64_t mb = static_cast<uint64_t>(__double_as_longlong(M.b));
+    return kSane && (!eat || mb - 0x2050000000000000ull <= 0x3F00000000000000ull);
 }
 
 // ---------------------------------------------------------------------------
@@ -700,6 +720,69 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(cons
 // slot, and the slots are folded in tile order, so the sums stay
 // deterministic.  Odd steps claim tiles from the end, so the front runs
 // backwards over the lines the previous step wrote last (L2 reuse).
+#ifndef FSB_DYN_FAST
+#define FSB_DYN_FAST 1  // A/B: 0 = the guarded loop (ok flags, warp vote, fallback call) in in-range mode too
+#endif
+// The claimed-tile loop of step_kernel_dyn for one warp (see there).  kFast:
+// in-range state and divisor, no guards and no fallback call in the loop.
+template <bool kExplicitCur, bool kSane, bool kFast>
+__device__ __forceinline__ void dyn_tiles(const StepArgs& a, const StepParams& P, bool eat, const SharedDivisor& M,
+                                          uint64_t step, bool rev, Partial* tile_part, unsigned& next_tile,
+                                          const unsigned& s_ghi, const unsigned& s_gpt, const unsigned& s_ntiles) {
+    const uint64_t npairs = a.n >> 1;
+    double2* X2 = reinterpret_cast<double2*>(a.s.x);
+    double2* Y2 = reinterpret_cast<double2*>(a.s.y);
+    double2* W2 = reinterpret_cast<double2*>(a.s.w);
+    double2* P2 = reinterpret_cast<double2*>(a.s.p);
+    const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
+    const SoA2 src{X2, Y2, W2, P2, C2};
+    const unsigned lane = threadIdx.x & 31;
+    // one loop over groups; a warp claims its next tile when the current one
+    // is exhausted (warp-uniform branch), flushing the finished tile's partial
+    unsigned grp = 0, gend = 0, tile = ~0u;
+    Partial acc = identity();
+    for (;;) {
+        if (grp == gend) {
+            if (tile != ~0u) {
+                const Partial tp = warp_reduce(acc);
+                if (lane == 0) tile_part[tile] = tp;
+                acc = identity();
+            }
+            unsigned claim = 0;
+            if (lane == 0) claim = atomicAdd(&next_tile, 1u);
+            claim = __shfl_sync(0xffffffffu, claim, 0);
+            const unsigned nt = *(volatile const unsigned*)&s_ntiles;
+            if (claim >= nt) break;
+            tile = rev ? nt - 1 - claim : claim;
+            FSB_CHECK(nt <= (unsigned)kDynTiles && tile < nt);
+            const unsigned gpt_ = *(volatile const unsigned*)&s_gpt;
+            const unsigned gh = *(volatile const unsigned*)&s_ghi;
+            grp = (tile * gridDim.x + blockIdx.x) * gpt_;
+            gend = (grp + gpt_ < gh) ? grp + gpt_ : gh;
+        }
+        const uint64_t q = (uint64_t)grp * 32 + lane;
+        double2 X[1], Y[1], W[1], Q[1], C[1];
+        const bool valid[1] = {q < npairs};
+        const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
+        if (valid[0]) {
+            X[0] = X2[q];
+            Y[0] = Y2[q];
+            W[0] = W2[q];
+            Q[0] = P2[q];
+            if (kExplicitCur) C[0] = C2[q];
+        }
+        fused_pairs<kExplicitCur, 1, kSane, true, false, false, kFast>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M,
+                                                                       step, acc);
+        if (valid[0]) {
+            X2[q] = X[0];
+            Y2[q] = Y[0];
+            W2[q] = W[0];
+            P2[q] = Q[0];
+        }
+        ++grp;
+    }
+}
+
 template <bool kExplicitCur, bool kSane>
 __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_dyn(const StepArgs a) {
     __shared__ Partial tile_part[kDynTiles];
@@ -734,56 +817,11 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     }
     __syncthreads();
 
-    double2* X2 = reinterpret_cast<double2*>(a.s.x);
-    double2* Y2 = reinterpret_cast<double2*>(a.s.y);
-    double2* W2 = reinterpret_cast<double2*>(a.s.w);
-    double2* P2 = reinterpret_cast<double2*>(a.s.p);
-    const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
-    const SoA2 src{X2, Y2, W2, P2, C2};
     const unsigned lane = threadIdx.x & 31;
-    // one loop over groups; a warp claims its next tile when the current one
-    // is exhausted (warp-uniform branch), flushing the finished tile's partial
-    unsigned grp = 0, gend = 0, tile = ~0u;
-    Partial acc = identity();
-    for (;;) {
-        if (grp == gend) {
-            if (tile != ~0u) {
-                const Partial tp = warp_reduce(acc);
-                if (lane == 0) tile_part[tile] = tp;
-                acc = identity();
-            }
-            unsigned claim = 0;
-            if (lane == 0) claim = atomicAdd(&next_tile, 1u);
-            claim = __shfl_sync(0xffffffffu, claim, 0);
-            const unsigned nt = *(volatile unsigned*)&s_ntiles;
-            if (claim >= nt) break;
-            tile = rev ? nt - 1 - claim : claim;
-            FSB_CHECK(nt <= (unsigned)kDynTiles && tile < nt);
-            const unsigned gpt_ = *(volatile unsigned*)&s_gpt;
-            const unsigned gh = *(volatile unsigned*)&s_ghi;
-            grp = (tile * gridDim.x + blockIdx.x) * gpt_;
-            gend = (grp + gpt_ < gh) ? grp + gpt_ : gh;
-        }
-        const uint64_t q = (uint64_t)grp * 32 + lane;
-        double2 X[1], Y[1], W[1], Q[1], C[1];
-        const bool valid[1] = {q < npairs};
-        const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
-        if (valid[0]) {
-            X[0] = X2[q];
-            Y[0] = Y2[q];
-            W[0] = W2[q];
-            Q[0] = P2[q];
-            if (kExplicitCur) C[0] = C2[q];
-        }
-        fused_pairs<kExplicitCur, 1, kSane, true>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M, step, acc);
-        if (valid[0]) {
-            X2[q] = X[0];
-            Y2[q] = Y[0];
-            W2[q] = W[0];
-            P2[q] = Q[0];
-        }
-        ++grp;
-    }
+    if (FSB_DYN_FAST && no_guards<kSane>(eat, M))
+        dyn_tiles<kExplicitCur, kSane, true>(a, P, eat, M, step, rev, tile_part, next_tile, s_ghi, s_gpt, s_ntiles);
+    else
+        dyn_tiles<kExplicitCur, kSane, false>(a, P, eat, M, step, rev, tile_part, next_tile, s_ghi, s_gpt, s_ntiles);
     __syncthreads();
     const unsigned long long t_done = (a.ec.out && threadIdx.x == 0) ? gtimer() : 0ull;
     Partial cta = identity();
@@ -1192,13 +1230,6 @@ __device__ __forceinline__ void ws_compute(WsPair& f, const StepArgs& a, const S
     }
 }
 
-// In-range state and an in-range divisor (the global max, which other ranks'
-// states feed: checked once per step) leave nothing to guard.
-template <bool kSane>
-__device__ __forceinline__ bool ws_fast(bool eat, const SharedDivisor& M) {
-    const uint64_t mb = static_cast<uint64_t>(__double_as_longlong(M.b));
-    return kSane && (!eat || mb - 0x2050000000000000ull <= 0x3F00000000000000ull);
-}
 
 template <bool kSane, bool kFast>
 __device__ __forceinline__ void ws_consume(const StepArgs& a, const StepParams& P, bool eat, const SharedDivisor& M,
@@ -1273,7 +1304,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) step_kernel_ws(const StepArgs a
         }
     } else {
         const unsigned c = warp - 1;
-        if (ws_fast<kSane>(eat, M))
+        if (no_guards<kSane>(eat, M))
             ws_consume<kSane, true>(a, P, eat, M, step, R, c, g0, stride, rounds, acc);
         else
             ws_consume<kSane, false>(a, P, eat, M, step, R, c, g0, stride, rounds, acc);
