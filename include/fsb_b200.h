@@ -239,6 +239,15 @@ int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta);
  * A single rank connects to itself at creation. */
 int fsb_engine_peer_handle(fsb_engine* e, void* out, size_t len);
 int fsb_engine_peer_connect(fsb_engine* e, const void* handles, size_t len);
+/* The same for ranks that live in ONE process (one host thread or process
+ * driving several GPUs, SURVEY 8(b) "Threading"; or several shards of one GPU):
+ * ranks[q] is rank q's engine (ranks[e's rank] == e), every engine created with
+ * FSB_FLAG_PEER_EXCHANGE and the same world_size.  The windows are addressed by
+ * their device pointers; peer access is enabled between distinct devices.  Run
+ * and simulate launch kernels that wait for the other ranks' partials, so ranks
+ * sharing one GPU must use the phase API with every rank's move before any
+ * rank's eat (each call returns only when its kernels have finished). */
+int fsb_engine_peer_connect_local(fsb_engine* e, fsb_engine* const* ranks, int n);
 
 /* Host exchange (FSB_FLAG_HOST_EXCHANGE): the exchange step of eat_phase's
  * max (sim.hpp:110-114 -> executor.hpp:83-103), made explicit for callers

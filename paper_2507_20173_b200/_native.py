@@ -107,6 +107,7 @@ SIGNATURES = [
     ("fsb_engine_set_partials", _int, [_vp, _vp, _sz]),
     ("fsb_engine_peer_handle", _int, [_vp, _vp, _sz]),
     ("fsb_engine_peer_connect", _int, [_vp, _vp, _sz]),
+    ("fsb_engine_peer_connect_local", _int, [_vp, _vp, ctypes.c_int]),
     ("fsb_selftest_fast_math", _int, [_int, _u64, _u64, _vp]),
 ]
 

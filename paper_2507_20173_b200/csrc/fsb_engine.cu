@@ -1468,6 +1468,31 @@ extern "C" int fsb_engine_peer_handle(fsb_engine* e, void* out, size_t len) {
     return FSB_OK;
 }
 
+extern "C" int fsb_engine_peer_connect_local(fsb_engine* e, fsb_engine* const* ranks, int n) {
+    TRY(guard(e));
+    if (!e->peer_mode) return fail(FSB_ERR_INVALID_ARGUMENT, "engine not created with FSB_FLAG_PEER_EXCHANGE");
+    if (!ranks || n != e->world) return fail(FSB_ERR_INVALID_ARGUMENT, "need world_size engines");
+    if (ranks[e->rank] != e) return fail(FSB_ERR_INVALID_ARGUMENT, "ranks[rank] must be this engine");
+    std::vector<fsb_dev::PeerWindow*> peers(e->world);
+    for (int q = 0; q < e->world; ++q) {
+        const fsb_engine* r = ranks[q];
+        if (!r || !r->peer_mode || r->world != e->world || r->rank != q)
+            return fail(FSB_ERR_INVALID_ARGUMENT, "ranks[q] must be rank q's peer-exchange engine");
+        if (r->device != e->device) {
+            int ok = 0;
+            CU(cudaDeviceCanAccessPeer(&ok, e->device, r->device));
+            if (!ok) return fail(FSB_ERR_UNSUPPORTED, "no peer access between the ranks' devices");
+            const cudaError_t pe = cudaDeviceEnablePeerAccess(r->device, 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(pe, "peer access");
+            cudaGetLastError();
+        }
+        peers[q] = r->window;
+    }
+    CU(cudaMemcpy(e->d_peers, peers.data(), e->world * sizeof(fsb_dev::PeerWindow*), cudaMemcpyHostToDevice));
+    e->peer_connected = true;
+    return FSB_OK;
+}
+
 extern "C" int fsb_engine_peer_connect(fsb_engine* e, const void* handles, size_t len) {
     TRY(guard(e));
     if (!e->peer_mode) return fail(FSB_ERR_INVALID_ARGUMENT, "engine not created with FSB_FLAG_PEER_EXCHANGE");

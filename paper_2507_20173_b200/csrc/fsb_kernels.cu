@@ -35,6 +35,9 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef FSB_FAST_FENCE
+#define FSB_FAST_FENCE 1  // A/B: 0 = no RNG-first scheduling fence in the unguarded claimed-tile loop
+#endif
 #ifndef FSB_SPIN_ACQ
 #define FSB_SPIN_ACQ 0  // A/B: acquire load on every poll of a counter barrier
 #endif
@@ -515,7 +518,7 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
                 dep |= static_cast<unsigned>(b1);
             }
         }
-        dep = kPre ? 0u : (dep & static_cast<unsigned>(P.zero));
+        dep = (kPre || (kFast && !FSB_FAST_FENCE)) ? 0u : (dep & static_cast<unsigned>(P.zero));
         // the fence goes into high words (one LOP3 each)
         auto fenced = [dep](double v) {
             return __hiloint2double(__double2hiint(v) | static_cast<int>(dep), __double2loint(v));

@@ -250,6 +250,12 @@ class Engine:
         blob = b"".join(handles)
         N.check(N.lib().fsb_engine_peer_connect(self._h, blob, len(blob)))
 
+    def peer_connect_local(self, engines) -> None:
+        """Connect ranks that live in this process: `engines` = every rank's
+        Engine in rank order (fsb_engine_peer_connect_local)."""
+        arr = (ctypes.c_void_p * len(engines))(*[e._h.value for e in engines])
+        N.check(N.lib().fsb_engine_peer_connect_local(self._h, arr, len(engines)))
+
     def gather(self, local_idx) -> np.ndarray:
         """Fish at the given shard-local indices (Fish layout)."""
         idx = np.ascontiguousarray(local_idx, dtype=np.uint64)
