@@ -11,18 +11,28 @@
 //   step_kernel_dyn the same pass, one 1024-thread CTA per SM whose warps
 //                   claim tiles (round-robin stripes) and draw their RNG ahead
 //                   of the loaded state (the default from 3e6 fish: C1-C3).
+//   step_kernel_ws  the same pass warp-specialised: a cp.async.bulk producer
+//                   warp streams round buffers into shared memory for 31
+//                   consumer warps (FSB_FLAG_WS_TILES, opt-in).
 //   step_kernel_bulk  the same pass streamed through a shared-memory ring by
 //                   cp.async.bulk + mbarriers (FSB_FLAG_FORCE_BULK, A/B).
-//   grid_kernel     all T steps in one cooperative launch (FSB_FLAG_FLAT_GRID).
-//   cgrid_kernel    the same with 8-CTA clusters reducing over DSMEM before the
-//                   grid-wide exchange (FSB_STRATEGY_GRID; AUTO 16,385-2.5e6 fish).
+//   sgrid_kernel    all T steps in one cooperative launch with the school in
+//                   shared memory, one CTA per SM (FSB_STRATEGY_GRID; AUTO
+//                   16,385 to ~1.06e6 fish: C0).
+//   cgrid_kernel    all T steps in one cooperative launch of 8-CTA clusters,
+//                   the school in L2, reducing over DSMEM before the grid-wide
+//                   exchange (AUTO ~1.06e6-2.5e6 fish; FSB_FLAG_L2_GRID).
+//   grid_kernel     the same without clusters (FSB_FLAG_FLAT_GRID).
 //   eat_kernel      the trailing / standalone weight update (sim.hpp:115-121).
 //   reduce_kernel   max + sums of the current state without moving it (eat()
 //                   after an upload).
 //   cluster_kernel  small swarms: all T steps in one launch of one thread-block
-//                   cluster, state in registers, per-step reduction over DSMEM.
+//                   cluster, state in registers, per-step reduction over DSMEM
+//                   (AUTO up to 16,384 fish: C4).
 //   soa<->aos       Fish byte layout (sim.hpp:26-32) for upload / download.
 //
+// In-range runs (fsb_math.cuh) take unguarded instantiations of the hot loops:
+// no operand guards, no warp vote and no call to the exact fallback path.
 // Determinism: max is exact (any order).  The sums use a fixed tree for a
 // fixed (n, grid, step parity), so repeated runs are bit-identical.
 #include <cooperative_groups.h>
@@ -35,9 +45,6 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef FSB_FAST_FENCE
-#define FSB_FAST_FENCE 1  // A/B: 0 = no RNG-first scheduling fence in the unguarded claimed-tile loop
-#endif
 #ifndef FSB_SPIN_ACQ
 #define FSB_SPIN_ACQ 0  // A/B: acquire load on every poll of a counter barrier
 #endif
@@ -518,7 +525,7 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
                 dep |= static_cast<unsigned>(b1);
             }
         }
-        dep = (kPre || (kFast && !FSB_FAST_FENCE)) ? 0u : (dep & static_cast<unsigned>(P.zero));
+        dep = kPre ? 0u : (dep & static_cast<unsigned>(P.zero));
         // the fence goes into high words (one LOP3 each)
         auto fenced = [dep](double v) {
             return __hiloint2double(__double2hiint(v) | static_cast<int>(dep), __double2loint(v));
