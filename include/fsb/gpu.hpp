@@ -203,6 +203,12 @@ class Engine {
     void peer_connect(const std::vector<unsigned char>& all_handles) {
         check(fsb_engine_peer_connect(e_.get(), all_handles.data(), all_handles.size()));
     }
+    // Ranks of this process (one thread per GPU): every rank's engine in rank order.
+    void peer_connect_local(const std::vector<Engine*>& ranks) {
+        std::vector<fsb_engine*> h;
+        for (Engine* r : ranks) h.push_back(r ? r->e_.get() : nullptr);
+        check(fsb_engine_peer_connect_local(e_.get(), h.data(), static_cast<int>(h.size())));
+    }
     // CTA count of the step kernel for configuration sweeps (0 = automatic).
     void set_grid(int ctas) { check(fsb_engine_set_grid(e_.get(), ctas)); }
     int grid() const {

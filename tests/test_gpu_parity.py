@@ -557,14 +557,16 @@ def test_baseline_configs_every_step(golden_baseline, name):
             assert f"{eng.checksum():016x}" == want, f"after step {(k + 1) * every - 1}"
 
 
-def test_cpp_multi_gpu_example(golden_baseline):
+@pytest.mark.parametrize("mode", ["nccl", "peer"])
+def test_cpp_multi_gpu_example(golden_baseline, mode):
     """examples/simulate_multi_gpu (one host thread per GPU, C++ drop-in) on the
-    GPUs present: the chained shard checksum equals the reference C0 digest."""
+    GPUs present, exchanging by NCCL or by peer windows connected within the
+    process: the chained shard checksum equals the reference C0 digest."""
     exe = os.path.join(ROOT, "examples", "simulate_multi_gpu")
     if not os.path.exists(exe):
         subprocess.run(["make", "-s", "-C", os.path.dirname(exe)], check=True)
     g = golden_baseline["C0_1e6x100"]
-    r = subprocess.run([exe, str(fsb.device_count()), "1000000", "100", "7"], capture_output=True, text=True,
+    r = subprocess.run([exe, str(fsb.device_count()), "1000000", "100", "7", mode], capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0, r.stderr
     digest, last, _ = r.stdout.split()
