@@ -1864,7 +1864,7 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) cgrid_kernel(con
 // terminates the process on cooperative launches of clusters).
 constexpr unsigned kSGridMaxGrid = 160;  // warp 0 folds <= 5 partials per lane
 #ifndef FSB_SGRID_PAIRS
-#define FSB_SGRID_PAIRS 8
+#define FSB_SGRID_PAIRS 7  // x 512 threads x 148 CTAs x 2 = 1.06e6 fish, the shared-memory capacity anyway
 #endif
 #ifndef FSB_SGRID_U
 #define FSB_SGRID_U 1
@@ -1878,7 +1878,8 @@ constexpr bool kSGridPre = FSB_SGRID_PRE;     // keep fold_in(seed, fish) of the
 #ifndef FSB_SGRID_PREDRAW
 #define FSB_SGRID_PREDRAW 1
 #endif
-constexpr bool kSGridPreDraw = FSB_SGRID_PREDRAW;  // draw the first pair's next-step RNG during the barrier
+constexpr int kSGridPreDraw = FSB_SGRID_PREDRAW;  // pairs per thread whose next-step RNG is drawn during the barrier
+static_assert(kSGridPreDraw <= kSGridPairs && (!kSGridPreDraw || FSB_SGRID_PRE), "predraw needs the kept prefix");
 
 template <bool kSane, bool kBary>
 __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs g) {
@@ -1937,11 +1938,14 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
     double prev_best = -INFINITY;  // no pending eat at the start of a run
     // the next step's draws of the thread's first pair, made while the CTA waits
     // at the step's grid barrier (in-range runs; the draws need no max)
-    double pre[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double pre[kSGridPreDraw ? kSGridPreDraw : 1][2][2];
     auto predraw = [&](uint64_t nstep, bool more) {
-        if (kSane && kSGridPre && kSGridPreDraw && more && t < cnt) {
-            draw_ints(H[0][0], nstep, pre[0][0], pre[0][1]);
-            draw_ints(H[0][1], nstep, pre[1][0], pre[1][1]);
+#pragma unroll
+        for (int j = 0; j < kSGridPreDraw; ++j) {
+            if (kSane && kSGridPre && more && t + j * kSGridThreads < cnt) {
+                draw_ints(H[j][0], nstep, pre[j][0][0], pre[j][0][1]);
+                draw_ints(H[j][1], nstep, pre[j][1][0], pre[j][1][1]);
+            }
         }
     };
     for (uint64_t k = 0; k < g.num_steps; ++k) {
@@ -1974,11 +1978,11 @@ __global__ void __launch_bounds__(kSGridThreads, 1) sgrid_kernel(const SGridArgs
                     for (int u = 0; u < kSGridU; ++u) {
                         if (valid[u]) {
                             double m[2][2];
-                            if (kSGridPreDraw && j == 0 && u == 0 && k > 0) {  // drawn during the last barrier
-                                m[0][0] = pre[0][0];
-                                m[0][1] = pre[0][1];
-                                m[1][0] = pre[1][0];
-                                m[1][1] = pre[1][1];
+                            if (j + u < kSGridPreDraw && k > 0) {  // drawn during the last barrier
+                                m[0][0] = pre[j + u][0][0];
+                                m[0][1] = pre[j + u][0][1];
+                                m[1][0] = pre[j + u][1][0];
+                                m[1][1] = pre[j + u][1][1];
                             } else {
                                 draw_ints(H[kSGridPre ? j + u : 0][0], step, m[0][0], m[0][1]);
                                 draw_ints(H[kSGridPre ? j + u : 0][1], step, m[1][0], m[1][1]);

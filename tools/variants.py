@@ -88,6 +88,12 @@ VARIANTS = {
     "sg512u2np": ["-DFSB_SGRID_U=2", "-DFSB_SGRID_PRE=0"],
     "sg512np": ["-DFSB_SGRID_PRE=0"],
     "sgnopredraw": ["-DFSB_SGRID_PREDRAW=0"],
+    # shared-memory grid: pairs per thread (default 7) x pairs drawn during the barrier (default 1)
+    "sgp8d1": ["-DFSB_SGRID_PAIRS=8"],
+    "sgp7d2": ["-DFSB_SGRID_PREDRAW=2"],
+    "sgp8d2": ["-DFSB_SGRID_PAIRS=8", "-DFSB_SGRID_PREDRAW=2"],
+    "sgp8d3": ["-DFSB_SGRID_PAIRS=8", "-DFSB_SGRID_PREDRAW=3"],
+    "sgp8d4": ["-DFSB_SGRID_PAIRS=8", "-DFSB_SGRID_PREDRAW=4"],
     "sg1024np": ["-DFSB_SGRID_THREADS=1024", "-DFSB_SGRID_PAIRS=4", "-DFSB_SGRID_PRE=0"],
     "sg768u2np": ["-DFSB_SGRID_THREADS=768", "-DFSB_SGRID_PAIRS=5", "-DFSB_SGRID_U=2", "-DFSB_SGRID_PRE=0"],
     # claimed-tile kernel: minimum 32-pair groups per tile
