@@ -391,9 +391,13 @@ def test_long_stream_run_is_chunked(orc):
         assert eng.download().tobytes() == want_fish.tobytes()
 
 
-def test_run_split_equals_whole(orc):
-    cfg = fsb.baseline_config(40_000, 12)
-    with make(cfg, "stream") as a, make(cfg, "stream") as b:
+@pytest.mark.parametrize("strategy,kw", [("stream", {}), ("stream", {"ws_tiles": True}), ("grid", {}),
+                                         ("persistent", {})])
+def test_run_split_equals_whole(orc, strategy, kw):
+    """A run cut into pieces equals the whole run (each piece ends with its
+    trailing eat; the persistent kernels restart their per-step state)."""
+    cfg = fsb.baseline_config(4096 if strategy == "persistent" else 40_000, 12)
+    with make(cfg, strategy, **kw) as a, make(cfg, strategy, **kw) as b:
         a.init()
         b.init()
         ta, _, _ = a.run(0, 12)
@@ -404,7 +408,7 @@ def test_run_split_equals_whole(orc):
         assert a.download().tobytes() == b.download().tobytes()
 
 
-@pytest.mark.parametrize("strategy", STRATS)
+@pytest.mark.parametrize("strategy", STRATS + ["ws"])
 @pytest.mark.parametrize("first", [2**32 + 3, 2**63 + 7, 2**64 - 4])
 def test_large_step_index(orc, strategy, first):
     """The step index is a full u64 RNG word (rng.hpp:34-36): runs starting
@@ -413,7 +417,8 @@ def test_large_step_index(orc, strategy, first):
     cfg = fsb.baseline_config(n, 3)
     fish = orc.init(ocfg(cfg))
     want_trace = orc.run(ocfg(cfg), fish, first, 3)
-    with make(cfg, strategy) as eng:
+    kw = {"ws_tiles": True} if strategy == "ws" else {}
+    with make(cfg, "stream" if strategy == "ws" else strategy, **kw) as eng:
         eng.init()
         trace, _, _ = eng.run(first, 3)
         assert trace.tobytes() == want_trace.tobytes()
