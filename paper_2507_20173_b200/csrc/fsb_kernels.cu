@@ -1596,9 +1596,11 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
             }
         }
         Partial blk = identity();
-        if (kBary) blk = block_reduce(acc, scratch, kClock ? &t_done : nullptr, true);
-        else  // the CTA max travels as its key (bits in .best), decoded after the fold
+        if (kBary) {
+            blk = block_reduce(acc, scratch, kClock ? &t_done : nullptr, true);
+        } else {  // the CTA max travels as its key (bits in .best), decoded after the fold
             blk.best = __longlong_as_double(static_cast<long long>(block_max_key(max_key(acc.best), scratch_key, kClock ? &t_done : nullptr, true)));
+        }
         if (threadIdx.x < 32 && threadIdx.x < ncta) {  // lane r pushes this CTA's partial to CTA r
             const uint32_t dst = cluster_map(smem_u32(&slots[b][crank]), threadIdx.x);
             const uint32_t bar = cluster_map(smem_u32(&xbar[b]), threadIdx.x);
