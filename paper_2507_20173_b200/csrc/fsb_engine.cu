@@ -193,6 +193,7 @@ struct fsb_engine {
     fsb_dev::PeerWindow** d_peers = nullptr;  // [world] device array of mapped windows
     std::vector<void*> opened;               // IPC mappings to close
     uint64_t xseq = 0;                       // exchanges completed (epoch of the latest)
+    unsigned long long peer_timeout_ns = 60000000000ull;  // a kernel's wait for the other ranks' partials
 };
 
 namespace {
@@ -320,6 +321,7 @@ fsb_dev::PeerXchg px_of(const fsb_engine* e, const uint64_t* seq_ptr, uint64_t i
     px.seq_ptr = seq_ptr;
     px.in_add = in_add;
     px.out_add = out_add;
+    px.timeout_ns = e->peer_timeout_ns;
     return px;
 }
 
@@ -331,6 +333,19 @@ int need_peers(const fsb_engine* e) {
 
 // Host exchange with more than one rank: the caller's partials must be in place.
 bool host_multi(const fsb_engine* e) { return e->host_xchg && e->world > 1; }
+
+// Peer exchange failure detection: a kernel that waited longer than the
+// device-side timeout for another rank's partial marked its window (the call's
+// results are void).  Checked after every call that consumes partials.
+int peer_fault(fsb_engine* e) {
+    if (!e->peer_mode || !e->window) return FSB_OK;
+    unsigned long long f = 0;
+    CU(cudaMemcpy(&f, &e->window->fault, sizeof f, cudaMemcpyDeviceToHost));
+    if (!f) return FSB_OK;
+    CU(cudaMemset(&e->window->fault, 0, sizeof f));
+    return fail(FSB_ERR_NCCL, "peer exchange: the partials of epoch " + std::to_string(f) +
+                                  " did not all arrive (a rank stopped publishing); results void");
+}
 
 int need_partials(const fsb_engine* e) {
     if (host_multi(e) && !e->xchg_ready)
@@ -506,6 +521,7 @@ int run_stream(fsb_engine* e, uint64_t first_step, uint64_t T, double* trace, do
     if (trace) CU(cudaMemcpyAsync(trace, it->second.d_trace, T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     if (bary) CU(cudaMemcpyAsync(bary, it->second.d_bary, 3 * T * sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     CU(cudaStreamSynchronize(e->stream));
+    TRY(peer_fault(e));
     TRY(elapsed(e, seconds));
     TRY(read_eat_ns(e, 1.0, &e->last_eat_s));
     e->cur_explicit = false;
@@ -936,6 +952,10 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     CB(cudaMallocHost(&e->h_step0, 2 * sizeof(uint64_t)));
     if (e->peer_mode) {
         if (e->world > fsb_dev::kMaxRanks) return bail(fail(FSB_ERR_UNSUPPORTED, "peer exchange: too many ranks"));
+        if (const char* v = std::getenv("FSB_PEER_TIMEOUT_S")) {  // failure-detection horizon (default 60 s)
+            const double sec = std::atof(v);
+            if (sec > 0) e->peer_timeout_ns = (unsigned long long)(sec * 1e9);
+        }
         CB(cudaMalloc(&e->window, sizeof(fsb_dev::PeerWindow)));
         CB(cudaMemset(e->window, 0, sizeof(fsb_dev::PeerWindow)));
         CB(cudaMalloc(&e->d_peers, e->world * sizeof(fsb_dev::PeerWindow*)));
@@ -1128,6 +1148,7 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds) {
     double m = 0.0;
     CU(cudaMemcpyAsync(&m, e->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, e->stream));
     CU(cudaStreamSynchronize(e->stream));
+    TRY(peer_fault(e));
     // EatResult::seconds (sim.hpp:103): the max only, not the weight update
     TRY(read_eat_ns(e, 1.0, &e->last_eat_s));
     if (seconds) *seconds = e->last_eat_s;

@@ -39,6 +39,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 
 #include "fsb_kernels.cuh"
 #include "fsb_math.cuh"
@@ -272,8 +273,23 @@ __device__ __forceinline__ Partial wait_and_combine_peers(const PeerXchg& px, in
     PeerWindow* w = px.local;
     if (threadIdx.x == 0) {
         Partial r = identity();
-        for (int q = 0; q < world; ++q) {
-            while (ld_acquire_sys(&w->flags[b][q]) != epoch) __nanosleep(64);
+        const unsigned long long t0 = gtimer();
+        bool lost = false;
+        for (int q = 0; q < world && !lost; ++q) {
+            while (ld_acquire_sys(&w->flags[b][q]) != epoch) {
+                __nanosleep(64);
+                // failure detection: a rank that never publishes (crashed, or not
+                // launched) must not hang this GPU: give up, mark the window for
+                // the host (the call fails), and combine nothing -- no max, so
+                // this kernel applies no eat and a retry once the rank has
+                // published still gives the right state
+                if (gtimer() - t0 > px.timeout_ns) {
+                    w->fault = epoch;
+                    lost = true;
+                    break;
+                }
+            }
+            if (lost) break;
             Partial v;
             v.best = ld_relaxed_sys(&w->slots[b][q].best);
             v.sx = ld_relaxed_sys(&w->slots[b][q].sx);
@@ -281,7 +297,7 @@ __device__ __forceinline__ Partial wait_and_combine_peers(const PeerXchg& px, in
             v.sf = ld_relaxed_sys(&w->slots[b][q].sf);
             fold(r, v);
         }
-        combined = r;
+        combined = lost ? identity() : r;
     }
     __syncthreads();
     return combined;

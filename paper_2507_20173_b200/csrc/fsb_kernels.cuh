@@ -142,6 +142,7 @@ constexpr int kMaxRanks = 64;
 struct PeerWindow {
     Partial slots[2][kMaxRanks];
     unsigned long long flags[2][kMaxRanks];
+    unsigned long long fault;  // nonzero: an epoch whose partials did not all arrive in time
 };
 
 struct PeerXchg {
@@ -151,6 +152,7 @@ struct PeerXchg {
     const uint64_t* seq_ptr;   // epoch base = (seq_ptr ? *seq_ptr : 0) ...
     uint64_t in_add;           // ... + in_add: epoch of the partials consumed (0 = none)
     uint64_t out_add;          // ... + out_add: epoch of the partial produced (0 = none)
+    unsigned long long timeout_ns;  // give up waiting for a rank after this long (window.fault)
 };
 
 // Eat-region clock: the GPU counterpart of SimResult::seconds_eat, which the

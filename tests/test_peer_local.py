@@ -96,3 +96,30 @@ def test_peer_connect_local_errors():
     finally:
         for e in engs + [other, plain]:
             e.close()
+
+
+def test_peer_exchange_reports_a_rank_that_never_publishes(orc, monkeypatch):
+    """Failure detection: rank 1 never moves, so rank 0's eat kernel never sees
+    its partial; the kernel gives up after FSB_PEER_TIMEOUT_S (here 0.5 s; a
+    single bounded wait, no kernel waits on another), marks its window, and the
+    call fails with the NCCL/exchange error instead of hanging the GPU.  The
+    failed eat applied nothing, so once the late rank has published, the retry
+    gives the oracle's state."""
+    monkeypatch.setenv("FSB_PEER_TIMEOUT_S", "0.5")
+    cfg = fsb.baseline_config(10_000, 2)
+    engs = _ranks(cfg, 2)
+    try:
+        for e in engs:
+            e.init()
+        engs[0].move(0)
+        with pytest.raises(fsb.FsbError, match="did not all arrive"):
+            engs[0].eat()
+        engs[1].move(0)  # the late rank catches up: the exchange works again
+        m1, m0 = engs[1].eat().max_diff, engs[0].eat().max_diff
+        fish = orc.init(ocfg(cfg))
+        orc.move(ocfg(cfg), 0, fish)
+        assert bits(m0) == bits(m1) == bits(orc.eat(ocfg(cfg), fish))
+        assert np.concatenate([e.download() for e in engs]).tobytes() == fish.tobytes()
+    finally:
+        for e in engs:
+            e.close()
