@@ -230,6 +230,12 @@ int fsb_engine_last_strategy(const fsb_engine* e, int* strategy, const char** fa
  * fsb_engine_grid reports the grid in use and the threads per CTA. */
 int fsb_engine_set_grid(fsb_engine* e, int ctas);
 int fsb_engine_grid(const fsb_engine* e, int* ctas, int* threads_per_cta);
+/* Work granularity of the claimed-tile step kernel (the dynamic-schedule chunk
+ * of the reference's RunConfig, schedule.hpp; the gpu-exp2 sweep): the minimum
+ * number of 32-pair groups (64 fish) per tile a warp claims, 0 = the kernel's
+ * default (4).  Tiles are also never fewer than the shard needs to fit the
+ * kernel's 1024 tile slots per CTA.  Results do not depend on it. */
+int fsb_engine_set_tile_groups(fsb_engine* e, int groups);
 
 /* Peer exchange (FSB_FLAG_PEER_EXCHANGE, one process per GPU): each rank
  * exports its 64-byte CUDA IPC handle of its exchange window, the caller

@@ -121,6 +121,45 @@ def exp1(a, cfg) -> list:
     return recs
 
 
+# ---- Exp 2 analogue: work distribution x granularity --------------------------------
+# bench.hpp:103-127 sweeps the schedule kind (static / dynamic / guided) and its
+# chunk.  On the GPU: static chunks (one per CTA, the static-chunk kernel), warps
+# claiming tiles of 1..256 groups of 64 fish (the claimed-tile kernel: dynamic),
+# and the two shared-memory pipelines (the warp-specialised TMA kernel, the
+# bulk ring), each as the graph of step kernels.  chunk = fish per unit of work.
+def exp2(a, cfg) -> list:
+    plans = [("static", dict(static_tiles=True), None)]
+    plans += [("dynamic", dict(dynamic_tiles=True), g) for g in (1, 2, 4, 8, 16, 32, 64, 128, 256)]
+    plans += [("tma-ws", dict(ws_tiles=True), None), ("bulk-ring", dict(bulk=True), None)]
+    recs = []
+    for sched, kw, groups in plans:
+        try:
+            with sim.Engine(cfg, device=a.device, strategy="stream", **kw) as eng:
+                if groups is not None:
+                    eng.set_tile_groups(groups)
+                ctas, tpc = eng.grid()
+                if sched == "static":
+                    chunk = -(-cfg.num_fish // ctas)
+                elif sched == "dynamic":
+                    # tiles never fewer than the kernel's slots allow (fsb_engine_set_tile_groups)
+                    per = -(-((cfg.num_fish // 2 + 31) // 32) // (ctas * 1024))
+                    chunk = 64 * max(groups, per)
+                elif sched == "tma-ws":
+                    chunk = 31 * 64  # one round: 31 groups, one per consumer warp
+                else:
+                    chunk = 2 * 256  # one ring stage: 256 pairs
+                for r in range(a.warmup + a.reps):
+                    _, _, t = eng.simulate(barycentre=False)
+                    if r >= a.warmup:
+                        rec = _record("gpu-exp2", eng, cfg, t, r - a.warmup, construct="gpu-lastcta")
+                        rec.schedule, rec.chunk = sched, chunk
+                        recs.append(rec)
+        except Exception as e:
+            sys.stderr.write(f"gpu-exp2 {sched} {groups}: {e}\n")
+            recs.append(_failed("gpu-exp2", "gpu-lastcta", cfg, 1, schedule=sched))
+    return recs
+
+
 # ---- Exp 3 analogue: reduction constructs x G ---------------------------------------
 # (construct, engine kwargs, multi-rank capable)
 CONSTRUCTS = [
@@ -206,6 +245,8 @@ def cmd_gpuexp(a) -> int:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if a.exp in ("1", "all") and world == 1:
         recs += exp1(a, cfg)
+    if a.exp in ("2", "all") and world == 1:
+        recs += exp2(a, cfg)
     if a.exp in ("3", "all"):
         recs += exp3(a, cfg)
     if int(os.environ.get("RANK", "0")) != 0:
@@ -227,7 +268,7 @@ def main(argv=None) -> int:
         if name == "simulate":
             p.add_argument("--strategy", default="auto", choices=["auto", "stream", "persistent", "grid"])
         else:
-            p.add_argument("--exp", default="all", choices=["1", "3", "all"])
+            p.add_argument("--exp", default="all", choices=["1", "2", "3", "all"])
             p.add_argument("--reps", type=int, default=5)
             p.add_argument("--warmup", type=int, default=1)
     try:

@@ -102,6 +102,7 @@ SIGNATURES = [
     ("fsb_engine_last_launches", _int, [_vp, _P(_u64)]),
     ("fsb_engine_last_strategy", _int, [_vp, _P(_int), _P(ctypes.c_char_p)]),
     ("fsb_engine_set_grid", _int, [_vp, _int]),
+    ("fsb_engine_set_tile_groups", _int, [_vp, _int]),
     ("fsb_engine_grid", _int, [_vp, _P(_int), _P(_int)]),
     ("fsb_engine_partial", _int, [_vp, _vp]),
     ("fsb_engine_set_partials", _int, [_vp, _vp, _sz]),

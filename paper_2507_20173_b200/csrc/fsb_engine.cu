@@ -161,6 +161,7 @@ struct fsb_engine {
     int grid_aux = 0;        // grid of the eat / reduce kernels (SMs x occupancy, 256 threads)
     bool use_dyn = false;    // compact LDG step: step_kernel_dyn (one CTA per SM, claimed tiles)
     bool use_ws = false;     // compact step: step_kernel_ws (TMA producer warp, 31 consumer warps per SM)
+    unsigned tile_groups = 0;  // claimed-tile kernel: minimum groups per tile (0 = the kernel's default)
     int grid_coop = 0;       // grid of the cooperative persistent grid kernel
     unsigned long long* d_gen = nullptr;     // grid-kernel arrival counter
     int cgrid_nc = 0;                        // co-resident clusters of the cluster-reduced grid kernel (0: none)
@@ -430,6 +431,7 @@ fsb_dev::StepArgs step_args(fsb_engine* e, const fsb_dev::SoA& s) {
     a.bulk = e->use_bulk ? 1 : 0;
     a.dyn = e->use_dyn ? 1 : 0;
     a.wspec = e->use_ws ? 1 : 0;
+    a.tile_groups = e->tile_groups;
     a.sane = in_range(e) ? 1 : 0;
     return a;
 }
@@ -1433,6 +1435,14 @@ int fsb_engine_set_grid(fsb_engine* e, int ctas) {
     }
     if (g != e->grid) free_graphs(e);  // captured launches carry the old grid
     e->grid = g;
+    return FSB_OK;
+}
+
+int fsb_engine_set_tile_groups(fsb_engine* e, int groups) {
+    TRY(guard(e));
+    if (groups < 0 || groups > 4096) return fail(FSB_ERR_INVALID_ARGUMENT, "groups must be in [0, 4096]");
+    if ((unsigned)groups != e->tile_groups) free_graphs(e);  // captured launches carry the old value
+    e->tile_groups = (unsigned)groups;
     return FSB_OK;
 }
 

@@ -833,7 +833,8 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     // stripes of gpt groups dealt round-robin to the CTAs (tile k of this CTA
     // is stripe k * gridDim + blockIdx.x): every SM works on one moving front
     unsigned gpt = (unsigned)((ngroups_all + (uint64_t)gridDim.x * kDynTiles - 1) / ((uint64_t)gridDim.x * kDynTiles));
-    if (gpt < kDynMinGroups) gpt = kDynMinGroups;  // claims + tile flushes amortised over >= kDynMinGroups groups
+    const unsigned min_groups = a.tile_groups ? a.tile_groups : kDynMinGroups;
+    if (gpt < min_groups) gpt = min_groups;  // claims + tile flushes amortised over >= min_groups groups
     const unsigned nstripes = (unsigned)((ngroups_all + gpt - 1) / gpt);
     if (threadIdx.x == 0) {
         next_tile = 0;

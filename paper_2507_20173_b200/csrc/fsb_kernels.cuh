@@ -209,6 +209,7 @@ struct StepArgs {
     int sane;             // state and config in range: guards elided (fsb_math.cuh "In-range mode")
     int dyn;              // compact LDG path: step_kernel_dyn (one CTA per SM, claimed tiles)
     int wspec;            // compact path: step_kernel_ws (TMA producer warp + 31 consumer warps per SM)
+    unsigned tile_groups; // step_kernel_dyn: minimum 32-pair groups per claimed tile (0 = kDynMinGroups)
     EatLink ec;           // eat-region clock
 };
 

@@ -285,6 +285,10 @@ class Engine:
         """CTA count of the compact step / eat kernels (0 = automatic)."""
         N.check(N.lib().fsb_engine_set_grid(self._h, ctas))
 
+    def set_tile_groups(self, groups: int) -> None:
+        """Minimum 32-pair groups per claimed tile of the claimed-tile kernel (0 = default)."""
+        N.check(N.lib().fsb_engine_set_tile_groups(self._h, groups))
+
     def grid(self):
         """(CTAs, threads per CTA) of the compact step kernel in use."""
         c, t = ctypes.c_int(), ctypes.c_int()

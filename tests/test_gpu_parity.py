@@ -336,6 +336,21 @@ def test_grid_override_bit_exact(orc, kernel):
             eng.set_grid(-1)
 
 
+@pytest.mark.parametrize("groups", [1, 3, 64, 4096, 0])
+def test_tile_groups_bit_exact(orc, groups):
+    """fsb_engine_set_tile_groups (the gpu-exp2 granularity sweep): any claimed
+    tile size gives the oracle's state and trace."""
+    cfg = fsb.baseline_config(300_001, 5)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "stream", dynamic_tiles=True) as eng:
+        eng.set_tile_groups(groups)
+        trace, _, _ = eng.simulate(barycentre=False)
+        assert trace.tobytes() == want_trace.tobytes()
+        assert eng.download().tobytes() == want_fish.tobytes()
+        with pytest.raises(fsb.FsbError):
+            eng.set_tile_groups(-1)
+
+
 def test_dynamic_tiles_explicit_cur_and_repeatable(orc):
     """The claimed-tile kernel on its explicit-cur instantiation (first step
     after an inconsistent upload), and bitwise repeatability of its sums
@@ -635,6 +650,13 @@ def test_cli_simulate_record(tmp_path, capsys):
     assert len({r.checksum for r in exp1}) == 1 and not any(r.failed() for r in exp1)
     assert len(exp1) == 14 and len({r.chunk for r in exp1}) >= 5  # the fish-per-thread axis
     assert all(r.experiment == "gpu-exp1" and r.schedule == "graph" for r in exp1)
+    # Exp 2 (bench.hpp:103-127 analogue): static / dynamic tiles of 1..256 groups / TMA / bulk ring
+    assert cli_main(["gpuexp", "--exp", "2", "--fish", "1000001", "--steps", "6", "--reps", "1", "--warmup", "1",
+                     "--out", str(out)]) == 0
+    exp2 = records.read_csv(out.read_text())
+    assert len(exp2) == 12 and len({r.checksum for r in exp2}) == 1 and not any(r.failed() for r in exp2)
+    assert {r.schedule for r in exp2} == {"static", "dynamic", "tma-ws", "bulk-ring"}
+    assert len({r.chunk for r in exp2 if r.schedule == "dynamic"}) >= 6  # the granularity axis
     assert cli_main(["gpuexp", "--exp", "3", "--fish", "4096", "--steps", "50", "--reps", "2", "--warmup", "1",
                      "--out", str(out)]) == 0
     text = out.read_text()
