@@ -8,10 +8,13 @@ for failed cells (csv.hpp:30-36), checksum as 16 lowercase hex digits
                    the reference has OpenMP threads);
   * schedule     = the step loop the engine executed: "graph" (CUDA graph of
                    step kernels), "grid" (one cooperative grid for all steps),
-                   "cluster" (one thread-block cluster for all steps);
+                   "cluster" (one thread-block cluster for all steps); in the
+                   gpu-exp2 rows the work distribution of the step kernel
+                   instead: "static", "dynamic", "tma-ws", "bulk-ring";
   * chunk        = fish per GPU thread of the step kernel's grid
                    (fish / (GPUs x CTAs x threads per CTA), rounded up) -- the gpu-exp1
-                   sweep's axis;
+                   sweep's axis; in the gpu-exp2 rows the fish per unit of work
+                   (per CTA chunk, claimed tile, TMA round or ring stage);
   * construct    = "gpu" (simulate), or the reduction construct of the global
                    max in the gpu-exp3 rows (gpu-lastcta, gpu-nccl, gpu-peer,
                    gpu-smem-counter, gpu-cluster-slots, gpu-flat-counter,
