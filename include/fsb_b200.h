@@ -79,12 +79,14 @@ typedef struct fsb_timing {
 /* Step-loop strategies. */
 enum fsb_strategy {
     FSB_STRATEGY_AUTO = 0,       /* single GPU: persistent cluster up to 16384 fish, grid up to 2.5e6,
-                                    else stream */
+                                    else stream; several ranks: stream */
     FSB_STRATEGY_STREAM = 1,     /* one fused step kernel per step, CUDA-graph replayed  */
     FSB_STRATEGY_PERSISTENT = 2, /* one thread-block cluster runs all steps on chip       */
     FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps (single GPU,
                                     mid-size schools): up to ~1.06e6 fish the school lives in shared
-                                    memory (one CTA per SM, every CTA polls every CTA's slot); larger
+                                    memory (one CTA per SM, the CTAs meet at one arrival counter per
+                                    step; AUTO falls back to stream if the device refuses the
+                                    co-resident launch); larger
                                     schools stay in L2, CTAs reduce inside thread-block clusters and
                                     cluster leaders meet through one global slot each */
 };
