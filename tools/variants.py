@@ -82,6 +82,7 @@ VARIANTS = {
     "d640x2": ["-DFSB_DYN_THREADS=640", "-DFSB_DYN_MIN_BLOCKS=2"],
     # shared-memory grid kernel: threads per CTA x pairs per thread (x pairs per pass)
     "sg768": ["-DFSB_SGRID_THREADS=768", "-DFSB_SGRID_PAIRS=5"],
+    "sg640": ["-DFSB_SGRID_THREADS=640", "-DFSB_SGRID_PAIRS=6"],
     "sg512u2": ["-DFSB_SGRID_THREADS=512", "-DFSB_SGRID_PAIRS=8", "-DFSB_SGRID_U=2"],
     "sg1024": ["-DFSB_SGRID_THREADS=1024", "-DFSB_SGRID_PAIRS=4"],
     "spinacq": ["-DFSB_SPIN_ACQ=1"],
