@@ -46,9 +46,6 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef FSB_SPREAD_EXP
-#define FSB_SPREAD_EXP 0
-#endif
 #ifndef FSB_SPIN_ACQ
 #define FSB_SPIN_ACQ 0  // A/B: acquire load on every poll of a counter barrier
 #endif
@@ -320,7 +317,6 @@ __device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs&
         FSB_CHECK(blockIdx.x < ws.cap);
         store_partial(&ws.block_part[blockIdx.x], blk);
         if (ec_out) red_max_relaxed_gpu(&ec_out->t_done, t_done);  // ordered before the release below
-        if (FSB_SPREAD_EXP && ec_out) red_max_relaxed_gpu(&ec_out->t_first_inv, ~t_done);
         // release: this CTA's partial before its arrival; acquire: the last
         // arriver sees every partial (the counter's release sequence).  The
         // other threads of the last CTA are ordered after it by the barrier
@@ -385,12 +381,8 @@ __device__ __forceinline__ void publish_prev(const Partial& prev, double* trace_
             const EatStamp st = *ec.in;
             const unsigned long long region =
                 ec.phase ? (st.t_pub - st.t_done) + (t_have - t_start) : t_have - st.t_done;
-            if (FSB_SPREAD_EXP)  // TEMP experiment: the CTAs' done-time spread instead of the eat region
-                *ec.ns += st.t_done - ~st.t_first_inv;
-            else if (st.t_done && st.t_done <= st.t_pub && st.t_done <= t_have)
-                *ec.ns += region;
+            if (st.t_done && st.t_done <= st.t_pub && st.t_done <= t_have) *ec.ns += region;
             ec.in->t_done = 0ull;  // re-armed for the producer two steps on
-            ec.in->t_first_inv = 0ull;
         }
         if (trace_out) *trace_out = prev.best;
         if (bary_out) {

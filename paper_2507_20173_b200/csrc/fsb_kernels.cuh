@@ -172,8 +172,6 @@ struct PeerXchg {
 struct EatStamp {
     unsigned long long t_done;  // max over CTAs: all fish of the step updated
     unsigned long long t_pub;   // the step's rank partial published (last CTA)
-    unsigned long long t_first_inv;  // max over CTAs of ~t_done (FSB_SPREAD_EXP: the first CTA done)
-    unsigned long long pad;
 };
 struct EatClock {
     EatStamp s[2];              // by step parity (graph) / slot 0 (eager launches)

@@ -29,7 +29,9 @@ per-step timing build -- profiles/round2_ab_ws_variants.jsonl,
 profiles/round2_ab_wsgrid.jsonl, profiles/round2_wgrid_timing.txt; and the
 persistent cluster kernel's per-phase SM-cycle stamps (clock64 around the fish
 update, the block reduction and the DSMEM exchange of thread 0 of every CTA;
-method and numbers in profiles/round2_cluster_phases.txt).
+method and numbers in profiles/round2_cluster_phases.txt); and the step
+kernels' per-step CTA done-time spread (FSB_SPREAD_EXP with tools/cta_spread.py,
+sources at c84bfe5, profiles/round2_cta_done_spread.jsonl).
 """
 from __future__ import annotations
 
@@ -102,7 +104,6 @@ VARIANTS = {
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
     "dynguarded": ["-DFSB_DYN_FAST=0"],
-    "spread": ["-DFSB_SPREAD_EXP=1"],
     "dg16": ["-DFSB_DYN_MIN_GROUPS=16"],
     # warp-specialised kernel (FSB_FLAG_WS_TILES): round buffers in the ring
     "wsr2": ["-DFSB_WS_ROUNDS=2"],
