@@ -104,6 +104,7 @@ VARIANTS = {
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
     "dynguarded": ["-DFSB_DYN_FAST=0"],
+    "gclaim": ["-DFSB_GLOBAL_CLAIM=1"],
     "dg16": ["-DFSB_DYN_MIN_GROUPS=16"],
     # warp-specialised kernel (FSB_FLAG_WS_TILES): round buffers in the ring
     "wsr2": ["-DFSB_WS_ROUNDS=2"],
