@@ -948,8 +948,8 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     }
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
-    CB(cudaMalloc(&e->counter, 2 * sizeof(unsigned)));
-    CB(cudaMemset(e->counter, 0, 2 * sizeof(unsigned)));
+    CB(cudaMalloc(&e->counter, sizeof(unsigned)));
+    CB(cudaMemset(e->counter, 0, sizeof(unsigned)));
     CB(cudaMalloc(&e->d_step0, 2 * sizeof(uint64_t)));
     CB(cudaMallocHost(&e->h_step0, 2 * sizeof(uint64_t)));
     if (e->peer_mode) {

@@ -46,9 +46,6 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef FSB_GLOBAL_CLAIM
-#define FSB_GLOBAL_CLAIM 0
-#endif
 #ifndef FSB_SPIN_ACQ
 #define FSB_SPIN_ACQ 0  // A/B: acquire load on every poll of a counter barrier
 #endif
@@ -335,7 +332,6 @@ __device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs&
     if (threadIdx.x == 0) {
         store_partial(part_out, tot);
         *ws.counter = 0u;  // ready for the next launch
-        if (FSB_GLOBAL_CLAIM) ws.counter[1] = 0u;
         if (ec_out) ec_out->t_pub = gtimer();
     }
     const uint64_t epoch = px.peers ? epoch_of(px, px.out_add) : 0ull;
@@ -767,52 +763,6 @@ __device__ __forceinline__ void dyn_tiles(const StepArgs& a, const StepParams& P
     const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
     const SoA2 src{X2, Y2, W2, P2, C2};
     const unsigned lane = threadIdx.x & 31;
-#if FSB_GLOBAL_CLAIM
-    // TEMP experiment: tiles claimed from one global counter by every warp of
-    // the grid (inter-CTA balance); the sums lose their fixed order
-    {
-        unsigned* gctr = a.ws.counter + 1;
-        const unsigned gpt_ = *(volatile const unsigned*)&s_gpt;
-        const unsigned gh = *(volatile const unsigned*)&s_ghi;
-        const unsigned ntg = (gh + gpt_ - 1) / gpt_;
-        unsigned nxt = 0;
-        if (lane == 0) nxt = atomicAdd(gctr, 1u);
-        nxt = __shfl_sync(0xffffffffu, nxt, 0);
-        Partial acc = identity();
-        while (nxt < ntg) {
-            const unsigned t = rev ? ntg - 1 - nxt : nxt;
-            unsigned cn = 0;
-            if (lane == 0) cn = atomicAdd(gctr, 1u);  // the next claim in flight during this tile
-            const unsigned g0 = t * gpt_, g1 = (g0 + gpt_ < gh) ? g0 + gpt_ : gh;
-            for (unsigned grp = g0; grp < g1; ++grp) {
-                const uint64_t q = (uint64_t)grp * 32 + lane;
-                double2 X[1], Y[1], W[1], Q[1], C[1];
-                const bool valid[1] = {q < npairs};
-                const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
-                if (valid[0]) {
-                    X[0] = X2[q];
-                    Y[0] = Y2[q];
-                    W[0] = W2[q];
-                    Q[0] = P2[q];
-                    if (kExplicitCur) C[0] = C2[q];
-                }
-                fused_pairs<kExplicitCur, 1, kSane, true, false, false, kFast>(X, Y, W, Q, C, valid, src, qs, gi, P,
-                                                                               eat, M, step, acc);
-                if (valid[0]) {
-                    X2[q] = X[0];
-                    Y2[q] = Y[0];
-                    W2[q] = W[0];
-                    P2[q] = Q[0];
-                }
-            }
-            nxt = __shfl_sync(0xffffffffu, cn, 0);
-        }
-        const Partial wp = warp_reduce(acc);
-        if (lane == 0) tile_part[threadIdx.x >> 5] = wp;
-        if (threadIdx.x == 0) *const_cast<volatile unsigned*>(&s_ntiles) = blockDim.x >> 5;
-        return;
-    }
-#endif
     // one loop over groups; a warp claims its next tile when the current one
     // is exhausted (warp-uniform branch), flushing the finished tile's partial
     unsigned grp = 0, gend = 0, tile = ~0u;

@@ -31,7 +31,9 @@ persistent cluster kernel's per-phase SM-cycle stamps (clock64 around the fish
 update, the block reduction and the DSMEM exchange of thread 0 of every CTA;
 method and numbers in profiles/round2_cluster_phases.txt); and the step
 kernels' per-step CTA done-time spread (FSB_SPREAD_EXP with tools/cta_spread.py,
-sources at c84bfe5, profiles/round2_cta_done_spread.jsonl).
+sources at c84bfe5, profiles/round2_cta_done_spread.jsonl); tiles claimed from one global counter
+by every warp of the grid (FSB_GLOBAL_CLAIM with tools/gc_probe.py, sources at
+9291174, profiles/round2_ab_global_claim.txt).
 """
 from __future__ import annotations
 
@@ -104,7 +106,6 @@ VARIANTS = {
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
     "dynguarded": ["-DFSB_DYN_FAST=0"],
-    "gclaim": ["-DFSB_GLOBAL_CLAIM=1"],
     "dg16": ["-DFSB_DYN_MIN_GROUPS=16"],
     # warp-specialised kernel (FSB_FLAG_WS_TILES): round buffers in the ring
     "wsr2": ["-DFSB_WS_ROUNDS=2"],
