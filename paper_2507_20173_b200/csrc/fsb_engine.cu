@@ -1513,6 +1513,7 @@ extern "C" int fsb_engine_peer_connect_local(fsb_engine* e, fsb_engine* const* r
             int ok = 0;
             CU(cudaDeviceCanAccessPeer(&ok, e->device, r->device));
             if (!ok) return fail(FSB_ERR_UNSUPPORTED, "no peer access between the ranks' devices");
+            // guard() made this engine's device current: enable access from it
             const cudaError_t pe = cudaDeviceEnablePeerAccess(r->device, 0);
             if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(pe, "peer access");
             cudaGetLastError();
