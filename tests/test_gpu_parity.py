@@ -777,7 +777,8 @@ def test_phase_eat_seconds_is_the_max_only(orc):
 
 
 # ---- the shared-memory-resident grid (school on chip for all steps) ---------------
-@pytest.mark.parametrize("n,t", [(16_385, 7), (300_001, 5), (1_000_000, 4), (1_050_001, 3), (1_100_001, 3)])
+@pytest.mark.parametrize("n,t", [(16_385, 7), (300_001, 5), (1_000_000, 4), (1_050_001, 3), (1_060_864, 2),
+                                 (1_060_866, 2), (1_100_001, 3)])
 def test_smem_grid_and_l2_grid_bit_exact(orc, n, t):
     """Up to ~1.06e6 fish the grid strategy keeps every CTA's pairs in shared
     memory; past that (and with l2_grid) the L2-resident cluster grid runs.
