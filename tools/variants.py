@@ -29,7 +29,10 @@ per-step timing build -- profiles/round2_ab_ws_variants.jsonl,
 profiles/round2_ab_wsgrid.jsonl, profiles/round2_wgrid_timing.txt; and the
 persistent cluster kernel's per-phase SM-cycle stamps (clock64 around the fish
 update, the block reduction and the DSMEM exchange of thread 0 of every CTA;
-method and numbers in profiles/round2_cluster_phases.txt); and the step
+method and numbers in profiles/round2_cluster_phases.txt); the blocked
+[x|y|w|p] x 64-fish state layout (garbage-data timing probe at 068ec7c, 3 %
+faster; the full engine on real data, not committed, equal:
+profiles/round2_ab_blocked_layout_real_data.jsonl); and the step
 kernels' per-step CTA done-time spread (FSB_SPREAD_EXP with tools/cta_spread.py,
 sources at c84bfe5, profiles/round2_cta_done_spread.jsonl); tiles claimed from one global counter
 by every warp of the grid (FSB_GLOBAL_CLAIM with tools/gc_probe.py, sources at
