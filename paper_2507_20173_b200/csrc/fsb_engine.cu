@@ -901,11 +901,7 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     CB(cudaEventCreate(&e->ev0));
     CB(cudaEventCreate(&e->ev1));
     const size_t bytes = (e->count ? e->count : 1) * sizeof(double);
-#ifdef FSB_AOSOA_EXP
-    CB(cudaMalloc(&e->s.x, 4 * bytes + 4096));  // TEMP timing experiment: room for the interleaved blocks
-#else
     CB(cudaMalloc(&e->s.x, bytes));
-#endif
     CB(cudaMalloc(&e->s.y, bytes));
     CB(cudaMalloc(&e->s.w, bytes));
     CB(cudaMalloc(&e->s.p, bytes));

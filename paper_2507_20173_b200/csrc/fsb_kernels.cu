@@ -46,12 +46,6 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef FSB_FORCE_EAT_EXP
-#define FSB_FORCE_EAT_EXP 0  // TEMP timing experiment: the eat path on every step (garbage-data timing runs)
-#endif
-#ifndef FSB_AOSOA_EXP
-#define FSB_AOSOA_EXP 0
-#endif
 #ifndef FSB_SPIN_ACQ
 #define FSB_SPIN_ACQ 0  // A/B: acquire load on every poll of a counter barrier
 #endif
@@ -796,23 +790,6 @@ __device__ __forceinline__ void dyn_tiles(const StepArgs& a, const StepParams& P
         double2 X[1], Y[1], W[1], Q[1], C[1];
         const bool valid[1] = {q < npairs};
         const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
-#if FSB_AOSOA_EXP  // TEMP timing experiment: the four arrays interleaved per 32-pair group (x is 4x long)
-        double2* blk = X2 + (uint64_t)grp * 128 + lane;
-        if (valid[0]) {
-            X[0] = blk[0];
-            Y[0] = blk[32];
-            W[0] = blk[64];
-            Q[0] = blk[96];
-        }
-        fused_pairs<kExplicitCur, 1, kSane, true, false, false, kFast>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M,
-                                                                       step, acc);
-        if (valid[0]) {
-            blk[0] = X[0];
-            blk[32] = Y[0];
-            blk[64] = W[0];
-            blk[96] = Q[0];
-        }
-#else
         if (valid[0]) {
             X[0] = X2[q];
             Y[0] = Y2[q];
@@ -828,7 +805,6 @@ __device__ __forceinline__ void dyn_tiles(const StepArgs& a, const StepParams& P
             W2[q] = W[0];
             P2[q] = Q[0];
         }
-#endif
         ++grp;
     }
 }
@@ -844,7 +820,7 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     pdl_wait_and_release();
     const Partial prev = combine_prev(a.part_in, a.world, a.px);
     publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
-    const bool eat = FSB_FORCE_EAT_EXP || prev.best > 0.0;  // sim.hpp:115
+    const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
     const uint64_t n = a.n;

@@ -109,8 +109,6 @@ VARIANTS = {
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
     "dynguarded": ["-DFSB_DYN_FAST=0"],
-    "aosoa": ["-DFSB_AOSOA_EXP=1", "-DFSB_FORCE_EAT_EXP=1"],
-    "forceeat": ["-DFSB_FORCE_EAT_EXP=1"],
     "dg16": ["-DFSB_DYN_MIN_GROUPS=16"],
     # warp-specialised kernel (FSB_FLAG_WS_TILES): round buffers in the ring
     "wsr2": ["-DFSB_WS_ROUNDS=2"],
