@@ -795,3 +795,23 @@ def test_smem_grid_and_l2_grid_bit_exact(orc, n, t):
         assert got.tobytes() == want_fish.tobytes(), (n, l2)
         assert rel_ok(bary[-1], ref), (n, l2)
         assert 0.0 < tm.seconds_eat < tm.seconds_loop
+
+
+# ---- AUTO at its thresholds ----------------------------------------------------------
+@pytest.mark.parametrize("n,want", [(16_384, "persistent"), (16_385, "grid"), (2_500_000, "grid"),
+                                    (2_500_001, "stream"), (2_999_999, "stream"), (3_000_000, "stream")])
+def test_auto_thresholds_bit_exact(orc, n, want):
+    """AUTO's choice at each boundary (persistent cluster <= 16,384 fish < grid
+    <= 2.5e6 < graph of step kernels; static chunks < 3e6 <= claimed tiles):
+    the strategy it runs and the oracle's state and trace on both sides."""
+    cfg = fsb.baseline_config(n, 3)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    with make(cfg, "auto") as eng:
+        trace, bary, _ = eng.simulate(barycentre=True)
+        assert eng.last_strategy()[0] == want
+        got = eng.download()
+        ctas, tpc = eng.grid()
+        assert tpc == (1024 if n >= 3_000_000 else 256)  # the claimed-tile kernel from 3e6 fish
+    assert got.tobytes() == want_fish.tobytes()
+    assert trace.tobytes() == want_trace.tobytes()
+    assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
