@@ -254,7 +254,9 @@ int fsb_engine_peer_connect(fsb_engine* e, const void* handles, size_t len);
  * their device pointers; peer access is enabled between distinct devices.  Run
  * and simulate launch kernels that wait for the other ranks' partials, so ranks
  * sharing one GPU must use the phase API with every rank's move before any
- * rank's eat (each call returns only when its kernels have finished). */
+ * rank's eat (each call returns only when its kernels have finished).  The
+ * engines hold each other's window pointers: destroy them together, after the
+ * last call on any of them. */
 int fsb_engine_peer_connect_local(fsb_engine* e, fsb_engine* const* ranks, int n);
 
 /* Host exchange (FSB_FLAG_HOST_EXCHANGE): the exchange step of eat_phase's
