@@ -78,6 +78,9 @@ VARIANTS = {
     "c128": ["-DFSB_CLUSTER_MIN_FISH=128"],
     # persistent cluster / cluster-grid kernels: acquire at cluster scope on the DSMEM mbarrier waits
     "clacq": ["-DFSB_CLUSTER_ACQ=1"],
+    # persistent cluster kernel, max-only: every warp pushes its key to every CTA (no block barrier)
+    "clwp": ["-DFSB_CLUSTER_WPUSH=1"],
+    "clwp512": ["-DFSB_CLUSTER_WPUSH=1", "-DFSB_CLUSTER_WPUSH_SLOTS=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
     # persistent cluster kernel: fish per thread
     "cf2": ["-DFSB_CLUSTER_F=2"],
