@@ -1480,13 +1480,6 @@ constexpr int kMaxCluster = 16;
 #define FSB_CLUSTER_F 1
 #endif
 constexpr int kClusterF = FSB_CLUSTER_F;  // fish per thread of the persistent cluster kernel
-#ifndef FSB_CLUSTER_WPUSH
-#define FSB_CLUSTER_WPUSH 0
-#endif
-#ifndef FSB_CLUSTER_WPUSH_SLOTS
-#define FSB_CLUSTER_WPUSH_SLOTS 128
-#endif
-constexpr unsigned kWPushSlots = FSB_CLUSTER_WPUSH_SLOTS;
 
 __device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem, unsigned rank) {
     uint32_t r;
@@ -1497,12 +1490,6 @@ __device__ __forceinline__ uint32_t cluster_map(uint32_t local_smem, unsigned ra
 __device__ __forceinline__ void st_async_f64x2(uint32_t dst, double a, double b, uint32_t bar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(dst),
                  "d"(a), "d"(b), "r"(bar)
-                 : "memory");
-}
-
-__device__ __forceinline__ void st_async_u64(uint32_t dst, unsigned long long a, uint32_t bar) {
-    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(dst), "l"(a),
-                 "r"(bar)
                  : "memory");
 }
 
@@ -1556,17 +1543,6 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
     __shared__ Partial scratch[32];
     __shared__ unsigned long long scratch_key[32];
     constexpr unsigned kBytes = kBary ? 32 : 8;  // bytes each CTA pushes per destination
-#if FSB_CLUSTER_WPUSH
-    // max-only runs of up to kWPushSlots warps in the cluster: every WARP pushes its
-    // max key to every CTA (one exchange level, no block barrier)
-    __shared__ __align__(8) unsigned long long wslots[2][kWPushSlots];
-    const unsigned nwarp = blockDim.x >> 5;
-    const unsigned nslots = cluster.num_blocks() * nwarp;
-    const bool wpush = !kBary && nslots <= kWPushSlots;
-#else
-    constexpr bool wpush = false;
-    const unsigned nslots = 0;
-#endif
     if (threadIdx.x == 0) {
         mbar_init(&xbar[0], 1);
         mbar_init(&xbar[1], 1);
@@ -1612,7 +1588,7 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         const uint64_t step = a.first_step + k;
         const unsigned b = (unsigned)(k & 1);
         if (threadIdx.x == 0)
-            mbar_expect_tx(&xbar[b], wpush ? nslots * 8 : ncta * kBytes);  // may race the pushes: fine
+            mbar_expect_tx(&xbar[b], ncta * kBytes);  // may race the pushes: fine
         const bool eat = M > 0.0;
         const SharedDivisor D = make_divisor(eat ? M : 1.0);
         Partial acc = identity();
@@ -1637,22 +1613,12 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
             }
         }
         Partial blk = identity();
-#if FSB_CLUSTER_WPUSH
-        if (wpush) {  // lane r of every warp pushes the warp's max key to CTA r
-            const unsigned long long wk = warp_max_key(max_key(acc.best));
-            const unsigned lane = threadIdx.x & 31;
-            if (kClock && threadIdx.x == 0) t_done = clock64();
-            if (lane < ncta)
-                st_async_u64(cluster_map(smem_u32(&wslots[b][crank * nwarp + (threadIdx.x >> 5)]), lane), wk,
-                             cluster_map(smem_u32(&xbar[b]), lane));
-        } else
-#endif
         if (kBary) {
             blk = block_reduce(acc, scratch, kClock ? &t_done : nullptr, true);
         } else {  // the CTA max travels as its key (bits in .best), decoded after the fold
             blk.best = __longlong_as_double(static_cast<long long>(block_max_key(max_key(acc.best), scratch_key, kClock ? &t_done : nullptr, true)));
         }
-        if (!wpush && threadIdx.x < 32 && threadIdx.x < ncta) {  // lane r pushes this CTA's partial to CTA r
+        if (threadIdx.x < 32 && threadIdx.x < ncta) {  // lane r pushes this CTA's partial to CTA r
             const uint32_t dst = cluster_map(smem_u32(&slots[b][crank]), threadIdx.x);
             const uint32_t bar = cluster_map(smem_u32(&xbar[b]), threadIdx.x);
             if (kBary) {
@@ -1671,16 +1637,6 @@ __global__ void __launch_bounds__(1024) cluster_kernel(const ClusterArgs a) {
         mbar_wait_cluster(&xbar[b], (unsigned)((k >> 1) & 1));
         if (kClock && threadIdx.x == 0) ecl += clock64() - t_done;
         tot = identity();
-#if FSB_CLUSTER_WPUSH
-        if (wpush) {  // every warp folds all the warp keys itself
-            unsigned long long m = kKeyNegInf;
-            for (unsigned i = threadIdx.x & 31; i < nslots; i += 32) {
-                const unsigned long long v = wslots[b][i];
-                m = v > m ? v : m;
-            }
-            tot.best = key_value(warp_max_key(m));
-        } else
-#endif
         if (kBary) {  // every warp folds the <= 16 CTA partials itself (fixed butterfly)
             const unsigned lane = threadIdx.x & 31;
             tot = warp_reduce(lane < ncta ? slots[k & 1][lane] : identity());

@@ -36,7 +36,10 @@ profiles/round2_ab_blocked_layout_real_data.jsonl); and the step
 kernels' per-step CTA done-time spread (FSB_SPREAD_EXP with tools/cta_spread.py,
 sources at c84bfe5, profiles/round2_cta_done_spread.jsonl); tiles claimed from one global counter
 by every warp of the grid (FSB_GLOBAL_CLAIM with tools/gc_probe.py, sources at
-9291174, profiles/round2_ab_global_claim.txt).
+9291174, profiles/round2_ab_global_claim.txt); the persistent cluster kernel
+with one exchange level -- every warp pushes its max key to every CTA, no block
+barrier (FSB_CLUSTER_WPUSH, sources at 4a0a102,
+profiles/round2_ab_cluster_warp_push.jsonl).
 """
 from __future__ import annotations
 
@@ -78,9 +81,6 @@ VARIANTS = {
     "c128": ["-DFSB_CLUSTER_MIN_FISH=128"],
     # persistent cluster / cluster-grid kernels: acquire at cluster scope on the DSMEM mbarrier waits
     "clacq": ["-DFSB_CLUSTER_ACQ=1"],
-    # persistent cluster kernel, max-only: every warp pushes its key to every CTA (no block barrier)
-    "clwp": ["-DFSB_CLUSTER_WPUSH=1"],
-    "clwp512": ["-DFSB_CLUSTER_WPUSH=1", "-DFSB_CLUSTER_WPUSH_SLOTS=512"],
     "c1024": ["-DFSB_CLUSTER_MIN_FISH=1024"],
     # persistent cluster kernel: fish per thread
     "cf2": ["-DFSB_CLUSTER_F=2"],
