@@ -538,7 +538,7 @@ __device__ __forceinline__ void fused_pairs(double2 (&X)[U], double2 (&Y)[U], do
                 const uint64_t b1 = fold_in(h_step, 1);
                 U0[u][f] = __ull2double_rn(b0 >> 11);
                 U1[u][f] = __ull2double_rn(b1 >> 11);
-                dep |= static_cast<unsigned>(b1);
+                dep |= static_cast<unsigned>(b1 >> 11);  // a word the conversion computes anyway
             }
         }
         dep = kPre ? 0u : (dep & static_cast<unsigned>(P.zero));
@@ -749,9 +749,13 @@ __global__ void __launch_bounds__(kStepThreads, FSB_MIN_BLOCKS) step_kernel(cons
 #ifndef FSB_DYN_FAST
 #define FSB_DYN_FAST 1  // A/B: 0 = the guarded loop (ok flags, warp vote, fallback call) in in-range mode too
 #endif
+#ifndef FSB_DYN_FULL
+#define FSB_DYN_FULL 1  // A/B: 0 = the unguarded loop with 64-bit pair indices and the per-pair range predicate
+#endif
 // The claimed-tile loop of step_kernel_dyn for one warp (see there).  kFast:
 // in-range state and divisor, no guards and no fallback call in the loop.
-template <bool kExplicitCur, bool kSane, bool kFast>
+// kFull (with kFast): s_ghi counts full 32-pair groups only and the shard has fewer than 2^32 pairs.
+template <bool kExplicitCur, bool kSane, bool kFast, bool kFull = false>
 __device__ __forceinline__ void dyn_tiles(const StepArgs& a, const StepParams& P, bool eat, const SharedDivisor& M,
                                           uint64_t step, bool rev, Partial* tile_part, unsigned& next_tile,
                                           const unsigned& s_ghi, const unsigned& s_gpt, const unsigned& s_ntiles) {
@@ -767,6 +771,7 @@ __device__ __forceinline__ void dyn_tiles(const StepArgs& a, const StepParams& P
     // is exhausted (warp-uniform branch), flushing the finished tile's partial
     unsigned grp = 0, gend = 0, tile = ~0u;
     Partial acc = identity();
+    const bool live = P.zero == 0;  // true (see kFull below)
     for (;;) {
         if (grp == gend) {
             if (tile != ~0u) {
@@ -785,6 +790,36 @@ __device__ __forceinline__ void dyn_tiles(const StepArgs& a, const StepParams& P
             const unsigned gh = *(volatile const unsigned*)&s_ghi;
             grp = (tile * gridDim.x + blockIdx.x) * gpt_;
             gend = (grp + gpt_ < gh) ? grp + gpt_ : gh;
+        }
+        if (kFull) {
+            // Full groups only (the caller clipped s_ghi to them and takes the
+            // ragged last group itself), and fewer than 2^32 pairs: no range
+            // predicate, and every address is one IMAD.WIDE.U32 of a 32-bit index.
+            const unsigned q = grp * 32u + lane;
+            // `live` is always true but opaque to the compiler: the arithmetic stays in
+            // its own basic block behind the four loads.  With a compile-time-true
+            // predicate ptxas sinks the w and p loads into the RNG chains to save
+            // registers, and the step runs 6 % slower (profiles/round2_ab_dyn_full.jsonl).
+            double2 X[1], Y[1], W[1], Q[1], C[1];
+            const bool valid[1] = {live};
+            if (valid[0]) {
+                X[0] = X2[q];
+                Y[0] = Y2[q];
+                W[0] = W2[q];
+                Q[0] = P2[q];
+                if (kExplicitCur) C[0] = C2[q];
+            }
+            const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2ull * q};
+            fused_pairs<kExplicitCur, 1, kSane, true, false, false, kFast>(X, Y, W, Q, C, valid, src, qs, gi, P, eat,
+                                                                           M, step, acc);
+            if (valid[0]) {
+                X2[q] = X[0];
+                Y2[q] = Y[0];
+                W2[q] = W[0];
+                P2[q] = Q[0];
+            }
+            ++grp;
+            continue;
         }
         const uint64_t q = (uint64_t)grp * 32 + lane;
         double2 X[1], Y[1], W[1], Q[1], C[1];
@@ -829,7 +864,11 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
 
     // balanced contiguous chunk of 32-pair groups (32-bit group indices: up
     // to 2^37 fish per shard); tiles of gpt groups
-    const uint64_t ngroups_all = (npairs + 31) / 32;
+    // In-range launches of fewer than 2^32 pairs run the hot loop over FULL
+    // groups only; the ragged last group is warp 1 of CTA 0's (below).
+    const bool fast = FSB_DYN_FAST && no_guards<kSane>(eat, M);
+    const bool full = FSB_DYN_FULL && fast && (npairs >> 32) == 0;
+    const uint64_t ngroups_all = full ? npairs / 32 : (npairs + 31) / 32;
     // stripes of gpt groups dealt round-robin to the CTAs (tile k of this CTA
     // is stripe k * gridDim + blockIdx.x): every SM works on one moving front
     unsigned gpt = (unsigned)((ngroups_all + (uint64_t)gridDim.x * kDynTiles - 1) / ((uint64_t)gridDim.x * kDynTiles));
@@ -845,16 +884,52 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     __syncthreads();
 
     const unsigned lane = threadIdx.x & 31;
-    if (FSB_DYN_FAST && no_guards<kSane>(eat, M))
+    __shared__ Partial ragged_part;
+    if (full) {
+        dyn_tiles<kExplicitCur, kSane, true, true>(a, P, eat, M, step, rev, tile_part, next_tile, s_ghi, s_gpt,
+                                                   s_ntiles);
+        if (blockIdx.x == 0 && threadIdx.x >= 32 && threadIdx.x < 64 && (npairs & 31)) {  // the ragged last group
+            const uint64_t q = (npairs & ~31ull) + lane;
+            double2* X2 = reinterpret_cast<double2*>(a.s.x);
+            double2* Y2 = reinterpret_cast<double2*>(a.s.y);
+            double2* W2 = reinterpret_cast<double2*>(a.s.w);
+            double2* P2 = reinterpret_cast<double2*>(a.s.p);
+            const double2* C2 = reinterpret_cast<const double2*>(a.s.c);
+            const SoA2 src{X2, Y2, W2, P2, C2};
+            double2 X[1], Y[1], W[1], Q[1], C[1];
+            const bool valid[1] = {q < npairs};
+            const uint64_t qs[1] = {q}, gi[1] = {a.gfirst + 2 * q};
+            if (valid[0]) {
+                X[0] = X2[q];
+                Y[0] = Y2[q];
+                W[0] = W2[q];
+                Q[0] = P2[q];
+                if (kExplicitCur) C[0] = C2[q];
+            }
+            Partial racc = identity();
+            fused_pairs<kExplicitCur, 1, kSane, true, false, false, true>(X, Y, W, Q, C, valid, src, qs, gi, P, eat, M,
+                                                                          step, racc);
+            if (valid[0]) {
+                X2[q] = X[0];
+                Y2[q] = Y[0];
+                W2[q] = W[0];
+                P2[q] = Q[0];
+            }
+            racc = warp_reduce(racc);
+            if (lane == 0) ragged_part = racc;
+        }
+    } else if (fast) {
         dyn_tiles<kExplicitCur, kSane, true>(a, P, eat, M, step, rev, tile_part, next_tile, s_ghi, s_gpt, s_ntiles);
-    else
+    } else {
         dyn_tiles<kExplicitCur, kSane, false>(a, P, eat, M, step, rev, tile_part, next_tile, s_ghi, s_gpt, s_ntiles);
+    }
     __syncthreads();
     const unsigned long long t_done = (a.ec.out && threadIdx.x == 0) ? gtimer() : 0ull;
     Partial cta = identity();
     if (threadIdx.x < 32) {
         for (unsigned i = lane; i < s_ntiles; i += 32) fold(cta, tile_part[i]);
         cta = warp_reduce(cta);
+        if (full && blockIdx.x == 0 && (npairs & 31)) fold(cta, ragged_part);
         if ((n & 1ull) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail fish
             const uint64_t i = n - 1;
             double x = a.s.x[i], y = a.s.y[i], w = a.s.w[i], p = a.s.p[i];

@@ -40,6 +40,8 @@ by every warp of the grid (FSB_GLOBAL_CLAIM with tools/gc_probe.py, sources at
 with one exchange level -- every warp pushes its max key to every CTA, no block
 barrier (FSB_CLUSTER_WPUSH, sources at 4a0a102,
 profiles/round2_ab_cluster_warp_push.jsonl).
+Session 6: per-thread prefetch.global.L2 of the tile's next group(s) from the
+claimed-tile kernel's full-group loop (2-3 % slower, profiles/round2_ab_dyn_full.jsonl).
 """
 from __future__ import annotations
 
@@ -112,6 +114,8 @@ VARIANTS = {
     "dg2": ["-DFSB_DYN_MIN_GROUPS=2"],
     "dg8": ["-DFSB_DYN_MIN_GROUPS=8"],
     "dynguarded": ["-DFSB_DYN_FAST=0"],
+    # claimed-tile kernel: the unguarded loop with 64-bit pair indices and the per-pair range predicate
+    "dynfull0": ["-DFSB_DYN_FULL=0"],
     "dg16": ["-DFSB_DYN_MIN_GROUPS=16"],
     # warp-specialised kernel (FSB_FLAG_WS_TILES): round buffers in the ring
     "wsr2": ["-DFSB_WS_ROUNDS=2"],
