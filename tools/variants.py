@@ -41,7 +41,12 @@ with one exchange level -- every warp pushes its max key to every CTA, no block
 barrier (FSB_CLUSTER_WPUSH, sources at 4a0a102,
 profiles/round2_ab_cluster_warp_push.jsonl).
 Session 6: per-thread prefetch.global.L2 of the tile's next group(s) from the
-claimed-tile kernel's full-group loop (2-3 % slower, profiles/round2_ab_dyn_full.jsonl).
+claimed-tile kernel's full-group loop (2-3 % slower, profiles/round2_ab_dyn_full.jsonl);
+the warp-specialised kernel with software-pipelined consumers -- round r+1's
+RNG draws made in the same basic block as round r's fp64 arithmetic, at 1024 /
+896 / 768 threads per CTA (64 / 72 / 80 registers) -- bit-exact, equal to the
+plain kernel within noise (profiles/round2_ab_ws_pipe.jsonl): every structure
+lands on the same ~6.0 TB/s of moved bytes.
 """
 from __future__ import annotations
 
