@@ -102,7 +102,7 @@ enum fsb_strategy {
                                         itself (CUDA IPC windows) instead of an NCCL allgather */
 #define FSB_FLAG_STATIC_TILES 0x80u  /* LDG step kernel: one static chunk per 256-thread CTA, 4 CTAs per SM */
 #define FSB_FLAG_DYNAMIC_TILES 0x100u /* LDG step kernel: one 1024-thread CTA per SM whose warps claim tiles
-                                        (default: dynamic from 3e6 fish per shard) */
+                                        (default: dynamic at every shard size) */
 #define FSB_FLAG_FLAT_GRID 0x200u   /* FSB_STRATEGY_GRID without thread-block clusters (one counter barrier) */
 #define FSB_FLAG_HOST_EXCHANGE 0x400u /* world_size > 1 without NCCL: the caller moves the 4-scalar rank
                                         partials between move and eat (fsb_engine_partial /

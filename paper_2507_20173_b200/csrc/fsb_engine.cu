@@ -107,11 +107,12 @@ int nccl_fail(ncclResult_t r, const char* what) {
 }
 
 constexpr uint64_t kStagingFish = 1ull << 22;  // 160 MB AoS staging per chunk
-// Shards from this size take step_kernel_dyn: with the RNG drawn ahead of the
-// loaded state and tiles of >= 4 groups it is 1-6% faster than the static
-// chunks from 3e6 fish (C1 1e7: 111-114 vs 115-121 us), slower below
-// (profiles/r04_ab_dyn.jsonl).
-constexpr uint64_t kDynamicMinFish = 3000000;
+// Shards from this size take step_kernel_dyn.  Round 1 measured it ahead of
+// the static chunks only from 3e6 fish; with the unguarded full-group loop it
+// is 8-20 % faster at every size from 2e4 to 3e6 as well (1e6: 16.9 vs 21.0 us,
+// 2.75e6: 33.4 vs 39.8; profiles/round2_ab_dyn_vs_static.jsonl), so it is the
+// stream strategy's kernel at every size; FSB_FLAG_STATIC_TILES pins the other.
+constexpr uint64_t kDynamicMinFish = 0;
 
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
@@ -910,8 +911,7 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     // faster than the cp.async.bulk ring at 1e7 and 1e8 fish and 25% faster at
     // 1e6 (profiles/r03_ab_bulk_ldg.jsonl); the ring stays available for A/B.
     e->use_bulk = (e->flags & FSB_FLAG_FORCE_BULK) && !(e->flags & FSB_FLAG_NO_BULK);
-    // claimed tiles only where they measured faster (large shards); the
-    // static chunks win on L2-resident schools (profiles/r03_ab_kernels.jsonl)
+    // claimed tiles at every size (see kDynamicMinFish)
     e->use_dyn = !e->use_bulk && !(e->flags & FSB_FLAG_STATIC_TILES) &&
                  ((e->flags & FSB_FLAG_DYNAMIC_TILES) || e->count >= kDynamicMinFish);
     // the warp-specialised kernel replaces the claimed-tile one for the

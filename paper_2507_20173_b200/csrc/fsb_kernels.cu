@@ -7,10 +7,10 @@
 //                   max(prev-cur) (sim.hpp:112-114) plus the f-weighted
 //                   barycentre sums, reduced warp -> CTA -> grid (last CTA).
 //                   double2 loads/stores, two fish per thread; one static
-//                   chunk per 256-thread CTA (shards below 3e6 fish).
+//                   chunk per 256-thread CTA (FSB_FLAG_STATIC_TILES).
 //   step_kernel_dyn the same pass, one 1024-thread CTA per SM whose warps
 //                   claim tiles (round-robin stripes) and draw their RNG ahead
-//                   of the loaded state (the default from 3e6 fish: C1-C3).
+//                   of the loaded state (the stream strategy's default: C1-C3).
 //   step_kernel_ws  the same pass warp-specialised: a cp.async.bulk producer
 //                   warp streams round buffers into shared memory for 31
 //                   consumer warps (FSB_FLAG_WS_TILES, opt-in).

@@ -802,7 +802,7 @@ def test_smem_grid_and_l2_grid_bit_exact(orc, n, t):
                                     (2_500_001, "stream"), (2_999_999, "stream"), (3_000_000, "stream")])
 def test_auto_thresholds_bit_exact(orc, n, want):
     """AUTO's choice at each boundary (persistent cluster <= 16,384 fish < grid
-    <= 2.5e6 < graph of step kernels; static chunks < 3e6 <= claimed tiles):
+    <= 2.5e6 < graph of claimed-tile step kernels):
     the strategy it runs and the oracle's state and trace on both sides."""
     cfg = fsb.baseline_config(n, 3)
     want_fish, want_trace = orc.simulate(ocfg(cfg))
@@ -811,7 +811,7 @@ def test_auto_thresholds_bit_exact(orc, n, want):
         assert eng.last_strategy()[0] == want
         got = eng.download()
         ctas, tpc = eng.grid()
-        assert tpc == (1024 if n >= 3_000_000 else 256)  # the claimed-tile kernel from 3e6 fish
+        assert tpc == 1024  # the stream strategy's kernel is the claimed-tile one at every size
     assert got.tobytes() == want_fish.tobytes()
     assert trace.tobytes() == want_trace.tobytes()
     assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
