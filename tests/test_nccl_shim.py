@@ -24,7 +24,7 @@ import pytest
 
 import oracle
 import paper_2507_20173_b200 as fsb
-from conftest import ROOT
+from conftest import ROOT, bits, unhex
 
 pytestmark = pytest.mark.gpu
 
@@ -92,3 +92,53 @@ def test_world_gt1_graph_exchange_on_one_gpu(orc, n, steps, world, split, kw):
         assert ret[r][2] == ret[0][2], "ranks disagree on the barycentre sums"
         want = np.array(orc.barycentre_sums(want_fish))
         assert np.all(np.abs(bary[-1] - want) <= BARY_RTOL * np.abs(want))
+
+
+# ---- BASELINE's multi-GPU configs at full size (C2 G=2, C3 G in {2,4,8}) ----------
+def _config_worker(rank, world, uid, n, steps, barrier, ret):
+    """A rank of a full-size config: the whole run in one graph, then the FNV
+    checksum chained through the ranks in order (rank r continues from rank
+    r-1's state: the digest of the gathered school, sim.hpp:154-176)."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ["FSB_NCCL_LIB"] = SHIM
+    import paper_2507_20173_b200 as fsb_
+
+    cfg = fsb_.baseline_config(n, steps)
+    with fsb_.Engine(cfg, device=0, rank=rank, world_size=world, nccl_unique_id=uid) as e:
+        e.init()
+        trace, bary, _ = e.run(0, steps, barycentre=True)
+        ret[("trace", rank)] = trace.tobytes()
+        ret[("bary", rank)] = bary[-1].tobytes()
+        for r in range(world):
+            if r == rank:
+                ret["h"] = e.checksum(ret["h"]) if rank else e.checksum()
+            barrier.wait()
+
+
+@pytest.mark.parametrize("name,n,steps,world", [
+    ("C2_1e8x50", 10**8, 50, 2),
+    ("C3_1e9x20", 10**9, 20, 2),
+    ("C3_1e9x20", 10**9, 20, 4),
+    ("C3_1e9x20", 10**9, 20, 8),  # 1.25e8 fish per rank: the north_star's 8-GPU weak-scaling share
+])
+def test_baseline_multi_gpu_configs_sharded_on_one_gpu(golden_baseline, name, n, steps, world):
+    """The reference's digests (tests/golden/baseline_digests.json, made by the
+    unmodified reference): every step's max_diff on every rank, the final
+    checksum over the school gathered in rank order, the barycentre."""
+    import torch.multiprocessing as mp
+
+    g = golden_baseline[name]
+    uid = f"/fsb_nccl_shim_c{os.getpid()}_{time.time_ns()}".encode().ljust(128, b"\0")
+    mgr = mp.get_context("spawn").Manager()
+    ret, barrier = mgr.dict(), mgr.Barrier(world)
+    mp.start_processes(_config_worker, args=(world, uid, n, steps, barrier, ret), nprocs=world, join=True,
+                       start_method="spawn")
+    for r in range(world):
+        assert [bits(v) for v in np.frombuffer(ret[("trace", r)])] == g["trace_hex"], f"rank {r}: trace"
+        assert ret[("bary", r)] == ret[("bary", 0)]
+    assert f"{ret['h']:016x}" == g["final_checksum"]
+    want = np.array([unhex(v) for v in g["barycentre_fsum"]])
+    bary = np.frombuffer(ret[("bary", 0)])
+    assert np.all(np.abs(bary - want) <= BARY_RTOL * np.abs(want))
