@@ -131,3 +131,24 @@ def test_product_does_not_reference_oracle():
                 assert "import oracle" not in src and "liboracle" not in src and "fsb_oracle" not in src, f
     out = subprocess.run(["ldd", fsb.lib_path()], capture_output=True, text=True).stdout
     assert "oracle" not in out and "fsbref" not in out
+
+
+def test_nccl_shim_exports_the_entry_points_the_engine_loads():
+    """tests/cpp/libnccl_shim.so (test infrastructure for tests/test_nccl_shim.py)
+    must export exactly what fsb_engine.cu's nccl_load() dlsym()s, and name a
+    shared-memory object in its unique id."""
+    import ctypes
+
+    path = os.path.join(ROOT, "tests", "cpp", "libnccl_shim.so")
+    assert os.path.exists(path), "run __graft_entry__.build()"
+    shim = ctypes.CDLL(path)
+    src = open(os.path.join(ROOT, "paper_2507_20173_b200", "csrc", "fsb_engine.cu")).read()
+    import re
+
+    wanted = set(re.findall(r'dlsym\(h, "(nccl\w+)"\)', src))
+    assert wanted == {"ncclGetUniqueId", "ncclCommInitRank", "ncclCommDestroy", "ncclAllGather", "ncclGetErrorString"}
+    for name in wanted:
+        assert hasattr(shim, name), name
+    uid = ctypes.create_string_buffer(128)
+    assert shim.ncclGetUniqueId(uid) == 0
+    assert uid.value.startswith(b"/fsb_nccl_shim_")
