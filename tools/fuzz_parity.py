@@ -1,0 +1,80 @@
+#!/usr/bin/env python3
+"""Randomised parity sweep on the GPU box: random SimConfigs (school size, steps,
+seed, pond size, step length, weight scale -- including values far outside the
+BASELINE mapping, where walls clamp, weights saturate or the in-range fast
+paths do not apply) through a random engine choice (strategy, step kernel,
+alternation, checked mode, split runs), each compared with the CPU oracle:
+the downloaded school byte for byte, every step's max_diff bit for bit, the
+barycentre within 1e-12.  The oracle is the checker (tests/ and tools only).
+
+    python tools/fuzz_parity.py --cases 3000 --seed 1 > gpurun_out/fuzz.jsonl
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+import paper_2507_20173_b200 as fsb  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--cases", type=int, default=1000)
+ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--max-fish", type=int, default=300_000)
+args = ap.parse_args()
+rng = np.random.default_rng(args.seed)
+orc = oracle.Oracle()
+KERNELS = [{}, {"static_tiles": True}, {"dynamic_tiles": True}, {"ws_tiles": True}, {"bulk": True}]
+bad, t0 = 0, time.time()
+counts = {}
+for case in range(args.cases):
+    n = int(np.exp(rng.uniform(0, np.log(args.max_fish))))
+    steps = int(rng.integers(1, 13))
+    pond = float(2.0 ** rng.uniform(-3, 12)) if rng.random() < 0.7 else float(rng.uniform(1, 500))
+    # step lengths from a tiny fraction of the pond to several ponds (every move hits a wall)
+    step_base = pond * float(10.0 ** rng.uniform(-5, 0.7))
+    wscale = float(rng.choice([1.0, 1.5, 2.0, 10.0, float(2.0 ** rng.uniform(0, 8))]))
+    cfg = fsb.SimConfig(num_fish=n, pond_size=pond, weight_scale=wscale, num_steps=steps,
+                        seed=int(rng.integers(0, 2**64, dtype=np.uint64)), step_base=step_base)
+    strategy = str(rng.choice(["auto", "stream", "grid", "persistent"] if n <= 16384 else ["auto", "stream", "grid"]))
+    kw = dict(rng.choice(KERNELS)) if strategy == "stream" else {}
+    if strategy == "grid" and rng.random() < 0.3:
+        kw[str(rng.choice(["flat_grid", "l2_grid"]))] = True
+    kw["alternate"] = bool(rng.random() < 0.7)
+    if rng.random() < 0.15:
+        kw["checked"] = True
+    split = int(rng.integers(1, steps)) if steps > 1 and rng.random() < 0.3 else 0
+    ocfg = oracle.Config.make(num_fish=n, pond_size=pond, weight_scale=wscale, num_steps=steps, seed=cfg.seed,
+                              step_base=step_base)
+    want_fish, want_trace = orc.simulate(ocfg)
+    try:
+        with fsb.Engine(cfg, device=0, strategy=strategy, **kw) as eng:
+            eng.init()
+            if split:
+                a, ba, _ = eng.run(0, split, barycentre=True)
+                b, bb, _ = eng.run(split, steps - split, barycentre=True)
+                trace, bary = np.concatenate([a, b]), np.concatenate([ba, bb])
+            else:
+                trace, bary, _ = eng.run(0, steps, barycentre=True)
+            got = eng.download()
+            used = eng.last_strategy()[0]
+        want_b = np.array(orc.barycentre_sums(want_fish))
+        ok = (got.tobytes() == want_fish.tobytes() and trace.tobytes() == want_trace.tobytes()
+              and bool(np.all(np.abs(bary[-1] - want_b) <= 1e-12 * np.abs(want_b))))
+        err = ""
+    except Exception as ex:  # noqa: BLE001
+        ok, used, err = False, "?", repr(ex)
+    counts[used] = counts.get(used, 0) + 1
+    if not ok:
+        bad += 1
+        print(json.dumps({"case": case, "ok": False, "n": n, "steps": steps, "pond": pond, "step_base": step_base,
+                          "weight_scale": wscale, "seed": cfg.seed, "strategy": strategy, "kw": kw, "split": split,
+                          "error": err}), flush=True)
+print(json.dumps({"cases": args.cases, "rng_seed": args.seed, "mismatches": bad, "strategies_run": counts,
+                  "max_fish": args.max_fish, "seconds": round(time.time() - t0, 1)}), flush=True)
+sys.exit(1 if bad else 0)
