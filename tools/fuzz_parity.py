@@ -51,21 +51,48 @@ for case in range(args.cases):
     split = int(rng.integers(1, steps)) if steps > 1 and rng.random() < 0.3 else 0
     ocfg = oracle.Config.make(num_fish=n, pond_size=pond, weight_scale=wscale, num_steps=steps, seed=cfg.seed,
                               step_base=step_base)
-    want_fish, want_trace = orc.simulate(ocfg)
+    # a third of the cases start from an UPLOADED hand-built school instead of init: fish outside the pond,
+    # weights outside [1, w_max], arbitrary prev / current objectives (the explicit-cur kernels), special values
+    upload = None
+    first = 0
+    if rng.random() < 0.33 and n <= 50_000:
+        upload = np.zeros(n, dtype=oracle.FISH_DTYPE)
+        upload["x"] = rng.uniform(-0.2 * pond, 1.2 * pond, n)
+        upload["y"] = rng.uniform(-0.2 * pond, 1.2 * pond, n)
+        upload["weight"] = np.where(rng.random(n) < 0.5, 1.0, rng.uniform(0.25, 3.0 * cfg.weight_max(), n))
+        upload["prev_objective"] = rng.uniform(0, pond, n)
+        upload["current_objective"] = rng.uniform(0, pond, n)
+        special = np.array([0.0, -0.0, 5e-324, 1e-310, 1e300, pond / 2, pond, np.nextafter(pond, np.inf)])
+        for f in ("x", "y", "weight", "prev_objective", "current_objective"):
+            k = int(rng.integers(0, min(n, 8) + 1))
+            upload[f][rng.integers(0, n, k)] = rng.choice(special, k)
+        if rng.random() < 0.5:  # a consistent current objective: the compact kernels after an upload
+            for i in range(n):
+                upload["current_objective"][i] = orc.objective(upload["x"][i], upload["y"][i], pond)
+        first = int(rng.integers(0, 2**40))
+        want_fish = upload.copy()
+        want_trace = orc.run(ocfg, want_fish, first, steps)
+    else:
+        want_fish, want_trace = orc.simulate(ocfg)
     try:
         with fsb.Engine(cfg, device=0, strategy=strategy, **kw) as eng:
-            eng.init()
-            if split:
+            if upload is not None:
+                eng.upload(upload)
+                trace, bary, _ = eng.run(first, steps, barycentre=True)
+            elif split:
+                eng.init()
                 a, ba, _ = eng.run(0, split, barycentre=True)
                 b, bb, _ = eng.run(split, steps - split, barycentre=True)
                 trace, bary = np.concatenate([a, b]), np.concatenate([ba, bb])
             else:
+                eng.init()
                 trace, bary, _ = eng.run(0, steps, barycentre=True)
             got = eng.download()
             used = eng.last_strategy()[0]
         want_b = np.array(orc.barycentre_sums(want_fish))
-        ok = (got.tobytes() == want_fish.tobytes() and trace.tobytes() == want_trace.tobytes()
-              and bool(np.all(np.abs(bary[-1] - want_b) <= 1e-12 * np.abs(want_b))))
+        # (an uploaded school may hold 1e300 or non-finite sums: compare the barycentre only when it is finite)
+        bary_ok = (not np.all(np.isfinite(want_b))) or bool(np.all(np.abs(bary[-1] - want_b) <= 1e-12 * np.abs(want_b)))
+        ok = got.tobytes() == want_fish.tobytes() and trace.tobytes() == want_trace.tobytes() and bary_ok
         err = ""
     except Exception as ex:  # noqa: BLE001
         ok, used, err = False, "?", repr(ex)
@@ -74,6 +101,7 @@ for case in range(args.cases):
         bad += 1
         print(json.dumps({"case": case, "ok": False, "n": n, "steps": steps, "pond": pond, "step_base": step_base,
                           "weight_scale": wscale, "seed": cfg.seed, "strategy": strategy, "kw": kw, "split": split,
+                          "uploaded": upload is not None, "first_step": first,
                           "error": err}), flush=True)
 print(json.dumps({"cases": args.cases, "rng_seed": args.seed, "mismatches": bad, "strategies_run": counts,
                   "max_fish": args.max_fish, "seconds": round(time.time() - t0, 1)}), flush=True)
