@@ -26,6 +26,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cases", type=int, default=1000)
 ap.add_argument("--seed", type=int, default=1)
 ap.add_argument("--max-fish", type=int, default=300_000)
+ap.add_argument("--sharded", action="store_true",
+                help="every case as G = 2..8 shards on this GPU through the host exchange (fsb_engine_partial / "
+                     "set_partials between move and eat), the gathered school against the unsharded oracle")
 args = ap.parse_args()
 rng = np.random.default_rng(args.seed)
 orc = oracle.Oracle()
@@ -51,6 +54,40 @@ for case in range(args.cases):
     split = int(rng.integers(1, steps)) if steps > 1 and rng.random() < 0.3 else 0
     ocfg = oracle.Config.make(num_fish=n, pond_size=pond, weight_scale=wscale, num_steps=steps, seed=cfg.seed,
                               step_base=step_base)
+    if args.sharded:
+        world = int(rng.integers(2, 9))
+        skw = dict(rng.choice(KERNELS[:4]))
+        want_fish, want_trace = orc.simulate(ocfg)
+        try:
+            engs = [fsb.Engine(cfg, device=0, rank=r, world_size=world, host_exchange=True, **skw)
+                    for r in range(world)]
+            try:
+                for e in engs:
+                    e.init()
+                trace = []
+                for t in range(steps):
+                    for e in engs:
+                        e.move(t)
+                    parts = np.stack([e.partial() for e in engs])
+                    for e in engs:
+                        e.set_partials(parts)
+                    trace.append({e.eat().max_diff for e in engs})
+                got = b"".join(e.download().tobytes() for e in engs)
+            finally:
+                for e in engs:
+                    e.close()
+            ok = (got == want_fish.tobytes() and all(len(m) == 1 for m in trace)
+                  and np.array([m.pop() for m in trace]).tobytes() == want_trace.tobytes())
+            err = ""
+        except Exception as ex:  # noqa: BLE001
+            ok, err = False, repr(ex)
+        counts[f"G={world}"] = counts.get(f"G={world}", 0) + 1
+        if not ok:
+            bad += 1
+            print(json.dumps({"case": case, "ok": False, "n": n, "steps": steps, "pond": pond,
+                              "step_base": step_base, "weight_scale": wscale, "seed": cfg.seed, "world": world,
+                              "kw": skw, "error": err}), flush=True)
+        continue
     # a third of the cases start from an UPLOADED hand-built school instead of init: fish outside the pond,
     # weights outside [1, w_max], arbitrary prev / current objectives (the explicit-cur kernels), special values
     upload = None
