@@ -19,7 +19,9 @@ KERNELS = {
     "persistent": dict(strategy="persistent"),    # one thread-block cluster, state on chip
     "flatgrid": dict(strategy="grid", flat_grid=True),
     "bulk": dict(bulk=True),          # cp.async.bulk shared-memory ring
-    "ws": dict(ws_tiles=True),        # warp-specialised: TMA producer warp + 31 consumer warps
+    "ws": dict(ws_tiles=True),
+    "peer": dict(peer=True),          # the claimed-tile kernel with the peer-window exchange (world 1)
+    "peer": dict(peer=True),          # the claimed-tile kernel with the peer-window exchange (world 1)        # warp-specialised: TMA producer warp + 31 consumer warps
 }
 names = (sys.argv[1] if len(sys.argv) > 1 else "dyn,static,bulk").split(",")
 sizes = [(1_000_000, 100), (10_000_000, 100), (100_000_000, 20)]
