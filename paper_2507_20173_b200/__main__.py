@@ -17,7 +17,8 @@ one record each:
   * Exp 1 (thread scaling, bench.hpp:79-103): the step kernel's grid from an
     eighth of the SMs to 8 CTAs per SM -- the fish-per-thread axis (`chunk`);
   * Exp 3 (aggregation constructs, bench.hpp:132-148): the GPU's ways of
-    computing the step's global max -- last-CTA fold across a kernel
+    computing the step's global max -- a red.max key slot read across the
+    kernel boundary (the graph's default), the last-CTA fold across a kernel
     boundary, in-graph NCCL allgather, NVLink peer window, cluster DSMEM +
     leader slots, shared-memory grid counter barrier, flat counter barrier,
     REDUX + DSMEM in one cluster -- each with its eat-region time
@@ -151,7 +152,9 @@ def exp2(a, cfg) -> list:
                 for r in range(a.warmup + a.reps):
                     _, _, t = eng.simulate(barycentre=False)
                     if r >= a.warmup:
-                        rec = _record("gpu-exp2", eng, cfg, t, r - a.warmup, construct="gpu-lastcta")
+                        # the claimed-tile kernel's graph reduces by the key slot, the other kernels by the last CTA
+                        rec = _record("gpu-exp2", eng, cfg, t, r - a.warmup,
+                                      construct="gpu-keyslot" if sched == "dynamic" else "gpu-lastcta")
                         rec.schedule, rec.chunk = sched, chunk
                         recs.append(rec)
         except Exception as e:
@@ -163,7 +166,8 @@ def exp2(a, cfg) -> list:
 # ---- Exp 3 analogue: reduction constructs x G ---------------------------------------
 # (construct, engine kwargs, multi-rank capable)
 CONSTRUCTS = [
-    ("gpu-lastcta", dict(strategy="stream"), False),
+    ("gpu-keyslot", dict(strategy="stream"), False),  # the graph's default: split fold (red.max key per step)
+    ("gpu-lastcta", dict(strategy="stream", last_cta_fold=True), False),
     ("gpu-nccl", dict(strategy="stream", force_nccl=True), True),
     ("gpu-peer", dict(strategy="stream", peer=True), True),
     ("gpu-smem-counter", dict(strategy="grid"), False),

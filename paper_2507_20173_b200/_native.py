@@ -37,6 +37,7 @@ FLAG_FLAT_GRID = 0x200
 FLAG_HOST_EXCHANGE = 0x400
 FLAG_L2_GRID = 0x800
 FLAG_WS_TILES = 0x1000
+FLAG_LAST_CTA_FOLD = 0x2000
 
 
 class fsb_sim_config(ctypes.Structure):

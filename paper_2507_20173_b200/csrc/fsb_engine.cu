@@ -150,6 +150,11 @@ struct fsb_engine {
 
     Partial* part_all = nullptr;  // [2][world]
     Partial* block_part = nullptr;
+    // split fold of one-rank graph chains (fsb_kernels.cuh FastFold): three rotating key slots and
+    // two CTA-partial buffers of block_cap entries each
+    unsigned long long* ff_keys = nullptr;
+    Partial* ff_part = nullptr;
+    bool ff_enabled = true;  // off with FSB_FLAG_LAST_CTA_FOLD (or FSB_NO_SPLIT_FOLD=1 in the environment: A/B runs)
     unsigned* counter = nullptr;
     uint64_t* d_step0 = nullptr;  // [2]: first step of the launched graph, exchange epoch base
     uint64_t* h_step0 = nullptr;  // pinned [2], copied by each graph's first node
@@ -455,6 +460,17 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
     cudaError_t ce = cudaMemcpyAsync(e->d_step0, e->h_step0, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice,
                                      e->stream);
     if (ce == cudaSuccess) ce = cudaMemsetAsync(&e->eclk->ns, 0, sizeof(unsigned long long), e->stream);
+    // One rank, the claimed-tile kernel, no peer / host exchange: the split fold (FastFold).
+    const bool split = e->ff_enabled && T >= 1 && e->world == 1 && !e->use_nccl && !e->peer_mode && !e->host_xchg &&
+                       e->use_dyn && !e->use_ws && !e->use_bulk;
+    if (split && ce == cudaSuccess) ce = cudaMemsetAsync(e->ff_keys, 0, 3 * sizeof(unsigned long long), e->stream);
+    auto grid_of = [&](uint64_t k) { return (k == 0 && explicit_first) ? e->grid_explicit : e->grid; };
+    auto consume = [&](fsb_dev::FastFold& ff, uint64_t k) {  // the consumer of step k's partials
+        ff.key_in = e->ff_keys + k % 3;
+        ff.bp_in = e->ff_part + (k & 1) * (size_t)e->block_cap;
+        ff.bp_in_count = (unsigned)grid_of(k);
+        ff.fold_out = local_part(e, (int)(k & 1));
+    };
     uint64_t launches = 0;
     for (uint64_t k = 0; k < T && ce == cudaSuccess && rc == FSB_OK; ++k) {
         fsb_dev::SoA s = e->s;
@@ -469,6 +485,14 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         a.px = px_of(e, e->d_step0 + 1, k, k + 1);  // consumes epoch base+k, produces base+k+1
         a.pdl = (k > 0 && use_pdl(e)) ? 1 : 0;  // kernel -> kernel edges only
         a.ec = ec_link(e, (int)(k & 1), k ? (int)((k - 1) & 1) : -1, 0);
+        if (split) {
+            a.ff.key_out = e->ff_keys + k % 3;
+            a.ff.bp_out = e->ff_part + (k & 1) * (size_t)e->block_cap;
+            if (k) {
+                consume(a.ff, k - 1);
+                a.ff.key_reset = e->ff_keys + (k + 1) % 3;
+            }
+        }
         ce = fsb_dev::launch_step(a, (k == 0 && explicit_first) ? e->grid_explicit : e->grid, e->stream);
         ++launches;
         if (ce == cudaSuccess) rc = exchange(e, (int)(k & 1));
@@ -486,6 +510,7 @@ int build_graph(fsb_engine* e, uint64_t T, bool explicit_first, GraphEntry* out)
         ea.px = px_of(e, e->d_step0 + 1, T, 0);
         ea.pdl = use_pdl(e) ? 1 : 0;
         ea.ec = ec_link(e, -1, (int)((T - 1) & 1), 0);
+        if (split) consume(ea.ff, T - 1);
         ce = fsb_dev::launch_eat(ea, e->grid_aux, e->stream);
         ++launches;
     }
@@ -829,7 +854,7 @@ int fsb_engine_destroy(fsb_engine* e) {
     for (void* p : {(void*)e->s.x, (void*)e->s.y, (void*)e->s.w, (void*)e->s.p, (void*)e->c_buf,
                     (void*)e->part_all, (void*)e->block_part, (void*)e->counter, (void*)e->d_step0,
                     (void*)e->d_scalar, (void*)e->d_mismatch, e->staging, (void*)e->d_cl_trace,
-                    (void*)e->d_cl_bary, (void*)e->eclk})
+                    (void*)e->d_cl_bary, (void*)e->eclk, (void*)e->ff_keys, (void*)e->ff_part})
         if (p) cudaFree(p);
     if (e->h_step0) cudaFreeHost(e->h_step0);
     if (e->pinned) cudaFreeHost(e->pinned);
@@ -948,6 +973,12 @@ int fsb_engine_create(const fsb_sim_config* cfg, const fsb_engine_options* opts,
     }
     CB(cudaMalloc(&e->part_all, 2 * e->world * sizeof(Partial)));
     CB(cudaMalloc(&e->block_part, maxgrid * sizeof(Partial)));
+    CB(cudaMalloc(&e->ff_keys, 3 * sizeof(unsigned long long)));
+    CB(cudaMalloc(&e->ff_part, 2 * (size_t)maxgrid * sizeof(Partial)));
+    {
+        const char* off = std::getenv("FSB_NO_SPLIT_FOLD");
+        e->ff_enabled = !(off && *off && *off != '0') && !(e->flags & FSB_FLAG_LAST_CTA_FOLD);
+    }
     CB(cudaMalloc(&e->counter, sizeof(unsigned)));
     CB(cudaMemset(e->counter, 0, sizeof(unsigned)));
     CB(cudaMalloc(&e->d_step0, 2 * sizeof(uint64_t)));
@@ -1429,9 +1460,14 @@ int fsb_engine_set_grid(fsb_engine* e, int ctas) {
         CU(cudaStreamSynchronize(e->stream));
         Partial* nb = nullptr;
         CU(cudaMalloc(&nb, g * sizeof(Partial)));
+        Partial* nf = nullptr;
+        CU(cudaMalloc(&nf, 2 * (size_t)g * sizeof(Partial)));
         cudaFree(e->block_part);
+        cudaFree(e->ff_part);
         e->block_part = nb;
+        e->ff_part = nf;
         e->block_cap = g;
+        free_graphs(e);  // captured launches carry the old buffers
     }
     if (g != e->grid) free_graphs(e);  // captured launches carry the old grid
     e->grid = g;

@@ -310,9 +310,17 @@ __device__ __forceinline__ Partial wait_and_combine_peers(const PeerXchg& px, in
 // t_done (thread 0): when this CTA's fish were all updated (eat-region clock).
 __device__ __forceinline__ void grid_publish(const Partial& blk, const ReduceWs& ws, Partial* part_out,
                                              const PeerXchg& px, int world, EatStamp* ec_out,
-                                             unsigned long long t_done) {
+                                             unsigned long long t_done, const FastFold* ff = nullptr) {
     __shared__ Partial scratch[32];
     __shared__ bool am_last;
+    if (ff && ff->key_out) {  // split fold: nothing to wait for; the kernel boundary publishes both
+        if (threadIdx.x == 0) {
+            store_partial(&ff->bp_out[blockIdx.x], blk);
+            red_max_relaxed_gpu(ff->key_out, max_key(blk.best));
+            if (ec_out) red_max_relaxed_gpu(&ec_out->t_done, t_done);
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         FSB_CHECK(blockIdx.x < ws.cap);
         store_partial(&ws.block_part[blockIdx.x], blk);
@@ -381,7 +389,8 @@ __device__ __forceinline__ void publish_prev(const Partial& prev, double* trace_
             const EatStamp st = *ec.in;
             const unsigned long long region =
                 ec.phase ? (st.t_pub - st.t_done) + (t_have - t_start) : t_have - st.t_done;
-            if (st.t_done && st.t_done <= st.t_pub && st.t_done <= t_have) *ec.ns += region;
+            // (t_pub is the last CTA's publish stamp: used by the phase API only, absent with the split fold)
+            if (st.t_done && (!ec.phase || st.t_done <= st.t_pub) && st.t_done <= t_have) *ec.ns += region;
             ec.in->t_done = 0ull;  // re-armed for the producer two steps on
         }
         if (trace_out) *trace_out = prev.best;
@@ -390,6 +399,32 @@ __device__ __forceinline__ void publish_prev(const Partial& prev, double* trace_
             bary_out[1] = prev.sy;
             bary_out[2] = prev.sf;
         }
+    }
+}
+
+// Split fold, consumer side.  Every CTA: the previous step's max from its key
+// slot (after the kernel boundary; identity sums -- only the max feeds the eat).
+__device__ __forceinline__ Partial prev_from_key(const FastFold& ff) {
+    Partial r = identity();
+    r.best = key_value(__ldcg(ff.key_in));
+    return r;
+}
+// One warp of CTA 0: the CTA partials of the previous step folded in index order
+// (lane l takes l, l + 32, ...; then the fixed butterfly) into the rank partial
+// and the barycentre output; zeroes the next step's key slot.
+__device__ __forceinline__ void fold_prev_outputs(const FastFold& ff, double* bary_out) {
+    const unsigned lane = threadIdx.x & 31;
+    Partial f = identity();
+    for (unsigned i = lane; i < ff.bp_in_count; i += 32) fold(f, load_cg(&ff.bp_in[i]));
+    f = warp_reduce(f);
+    if (lane == 0) {
+        store_partial(ff.fold_out, f);
+        if (bary_out) {
+            bary_out[0] = f.sx;
+            bary_out[1] = f.sy;
+            bary_out[2] = f.sf;
+        }
+        if (ff.key_reset) *ff.key_reset = 0ull;
     }
 }
 
@@ -853,8 +888,9 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     const StepParams P = params_of(a.k);
     const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
     pdl_wait_and_release();
-    const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
+    const bool split = a.ff.key_in != nullptr;  // split fold: the max from its key slot, the sums folded beside the run
+    const Partial prev = split ? prev_from_key(a.ff) : combine_prev(a.part_in, a.world, a.px);
+    publish_prev(prev, a.trace_out, split ? nullptr : a.bary_out, a.ec, t_start);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
     const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
@@ -884,6 +920,9 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     __syncthreads();
 
     const unsigned lane = threadIdx.x & 31;
+    // the last warp of CTA 0 folds the previous step's CTA partials before it claims tiles (its
+    // share goes to the other warps)
+    if (split && blockIdx.x == 0 && threadIdx.x >= blockDim.x - 32) fold_prev_outputs(a.ff, a.bary_out);
     __shared__ Partial ragged_part;
     if (full) {
         dyn_tiles<kExplicitCur, kSane, true, true>(a, P, eat, M, step, rev, tile_part, next_tile, s_ghi, s_gpt,
@@ -943,7 +982,7 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
             fold(cta, tail);
         }
     }
-    grid_publish(cta, a.ws, a.part_out, a.px, a.world, a.ec.out, t_done);
+    grid_publish(cta, a.ws, a.part_out, a.px, a.world, a.ec.out, t_done, &a.ff);
 }
 
 // ---------------------------------------------------------------------------
@@ -1438,8 +1477,10 @@ template <bool kExplicitCur>
 __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
     const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
     pdl_wait_and_release();
-    const Partial prev = combine_prev(a.part_in, a.world, a.px);
-    publish_prev(prev, a.trace_out, a.bary_out, a.ec, t_start);
+    const bool split = a.ff.key_in != nullptr;
+    const Partial prev = split ? prev_from_key(a.ff) : combine_prev(a.part_in, a.world, a.px);
+    publish_prev(prev, a.trace_out, split ? nullptr : a.bary_out, a.ec, t_start);
+    if (split && blockIdx.x == 0 && threadIdx.x < 32) fold_prev_outputs(a.ff, a.bary_out);
     if (!(prev.best > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
     const SharedDivisor M = make_divisor(prev.best);
     const double half = a.k.half_pond;

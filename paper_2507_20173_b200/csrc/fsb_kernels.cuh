@@ -189,6 +189,26 @@ struct EatLink {
     int phase;                  // consumer mode: 1 = phase API (tail + own combine), 0 = graph chain
 };
 
+// Split fold of a one-rank graph chain (fsb_engine.cu build_graph): the next
+// step needs only the MAX of this step, so every CTA red.max's its max -- as an
+// order-preserving key -- into the step's key slot and stores its partial
+// without meeting the other CTAs (no arrival counter, no last-CTA fold inside
+// this kernel: two dependent L2 round trips and a block reduction off the
+// per-step chain).  The consumer (the next step kernel, or the trailing eat)
+// reads the key; one warp of its CTA 0 folds the CTA partials in index order
+// for the outputs (barycentre sums, the cached rank partial) beside the run.
+// Key slots rotate over three steps (CTA 0 of step k zeroes step k+1's slot,
+// last read by step k-1's consumers), CTA-partial buffers over two.
+struct FastFold {
+    unsigned long long* key_out;       // this step's key slot (nullptr: the last-CTA fold)
+    Partial* bp_out;                   // this step's CTA partials [gridDim.x]
+    const unsigned long long* key_in;  // the previous step's key slot (nullptr: nothing to consume this way)
+    const Partial* bp_in;              // the previous step's CTA partials
+    unsigned bp_in_count;              // CTAs of the kernel that produced them
+    Partial* fold_out;                 // where the folded partial of the previous step goes (the rank partial)
+    unsigned long long* key_reset;     // the next step's key slot, zeroed here (nullptr: none)
+};
+
 struct StepArgs {
     SoA s;
     Scalars k;
@@ -211,6 +231,7 @@ struct StepArgs {
     int wspec;            // compact path: step_kernel_ws (TMA producer warp + 31 consumer warps per SM)
     unsigned tile_groups; // step_kernel_dyn: minimum 32-pair groups per claimed tile (0 = kDynMinGroups)
     EatLink ec;           // eat-region clock
+    FastFold ff;          // split fold (step_kernel_dyn in a one-rank graph), all null otherwise
 };
 
 // Persistent cooperative-grid run (FSB_STRATEGY_GRID): `base` supplies the
@@ -279,6 +300,7 @@ struct EatArgs {
     int pdl;
     PeerXchg px;
     EatLink ec;
+    FastFold ff;  // consumer side only (key_in, bp_in, bp_in_count, fold_out)
 };
 
 struct ReduceArgs {

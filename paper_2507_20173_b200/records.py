@@ -16,7 +16,7 @@ for failed cells (csv.hpp:30-36), checksum as 16 lowercase hex digits
                    sweep's axis; in the gpu-exp2 rows the fish per unit of work
                    (per CTA chunk, claimed tile, TMA round or ring stage);
   * construct    = "gpu" (simulate), or the reduction construct of the global
-                   max in the gpu-exp3 rows (gpu-lastcta, gpu-nccl, gpu-peer,
+                   max in the gpu-exp3 rows (gpu-keyslot, gpu-lastcta, gpu-nccl, gpu-peer,
                    gpu-smem-counter, gpu-cluster-slots, gpu-flat-counter,
                    gpu-redux-dsmem);
   * seconds_eat  = SimResult::seconds_eat: the max region only, measured on

@@ -137,7 +137,7 @@ class Engine:
                  alternate: bool = True, force_nccl: bool = False, bulk=False, pdl: bool = True,
                  peer: bool = False, checked: bool = False, static_tiles: bool = False,
                  dynamic_tiles: bool = False, flat_grid: bool = False, host_exchange: bool = False,
-                 l2_grid: bool = False, ws_tiles: bool = False):
+                 l2_grid: bool = False, ws_tiles: bool = False, last_cta_fold: bool = False):
         self.cfg = cfg
         L = N.lib()
         self._uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
@@ -147,6 +147,7 @@ class Engine:
                  | (N.FLAG_CHECKED if checked else 0) | (N.FLAG_STATIC_TILES if static_tiles else 0)
                  | (N.FLAG_DYNAMIC_TILES if dynamic_tiles else 0) | (N.FLAG_FLAT_GRID if flat_grid else 0)
                  | (N.FLAG_HOST_EXCHANGE if host_exchange else 0) | (N.FLAG_L2_GRID if l2_grid else 0)
+                 | (N.FLAG_LAST_CTA_FOLD if last_cta_fold else 0)
                  | (N.FLAG_WS_TILES if ws_tiles else 0))
         opts = N.fsb_engine_options(device, rank, world_size,
                                     ctypes.cast(self._uid, ctypes.c_void_p) if self._uid else None,

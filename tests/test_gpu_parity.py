@@ -663,9 +663,9 @@ def test_cli_simulate_record(tmp_path, capsys):
     recs = records.read_csv(text)
     assert len({r.checksum for r in recs}) == 1 and not any(r.failed() for r in recs)
     exp3 = [r for r in recs if r.experiment == "gpu-exp3"]
-    assert {r.construct for r in exp3} == {"gpu-lastcta", "gpu-nccl", "gpu-peer", "gpu-smem-counter",
+    assert {r.construct for r in exp3} == {"gpu-keyslot", "gpu-lastcta", "gpu-nccl", "gpu-peer", "gpu-smem-counter",
                                           "gpu-cluster-slots", "gpu-flat-counter", "gpu-redux-dsmem"}
-    assert len(exp3) == 14 and all(r.threads == 1 for r in exp3)
+    assert len(exp3) == 16 and all(r.threads == 1 for r in exp3)
     assert {r.schedule for r in exp3} == {"graph", "grid", "cluster"}
     # Exp 3 rows carry a measured eat region (bench.hpp:132-148), valid for the reference's validate_records
     assert all(0.0 < r.seconds_eat < r.seconds_total for r in recs)
@@ -815,3 +815,28 @@ def test_auto_thresholds_bit_exact(orc, n, want):
     assert got.tobytes() == want_fish.tobytes()
     assert trace.tobytes() == want_trace.tobytes()
     assert rel_ok(bary[-1], orc.barycentre_sums(want_fish))
+
+
+# ---- the two per-step reductions of a one-rank graph ---------------------------------
+@pytest.mark.parametrize("n,t", [(1, 3), (63, 4), (100_003, 7), (3_000_001, 4)])
+def test_split_fold_equals_last_cta_fold(orc, n, t):
+    """The graph's default reduction (every CTA red.max's its max key into the
+    step's slot, the next kernel folds the sums beside its run: FastFold) and
+    FSB_FLAG_LAST_CTA_FOLD (arrival counter + last-CTA fold inside the kernel):
+    the oracle's school and trace from both, split runs included, the barycentre
+    within tolerance, the cached sums of the final state valid after the run."""
+    cfg = fsb.baseline_config(n, t)
+    want_fish, want_trace = orc.simulate(ocfg(cfg))
+    want_b = orc.barycentre_sums(want_fish)
+    for last_cta in (False, True):
+        with make(cfg, "stream", last_cta_fold=last_cta) as eng:
+            eng.init()
+            a, ba, tm = eng.run(0, 1, barycentre=True)
+            b, bb, _ = eng.run(1, t - 1, barycentre=True) if t > 1 else (a[:0], ba[:0], None)
+            trace, bary = np.concatenate([a, b]), np.concatenate([ba, bb])
+            assert trace.tobytes() == want_trace.tobytes(), last_cta
+            assert eng.download().tobytes() == want_fish.tobytes(), last_cta
+            assert rel_ok(bary[-1], want_b), last_cta
+            sums, _ = eng.barycentre()  # the rank partial the consumer folded
+            assert rel_ok(sums, want_b), last_cta
+            assert 0.0 < tm.seconds_eat < tm.seconds_loop
