@@ -412,19 +412,21 @@ __device__ __forceinline__ Partial prev_from_key(const FastFold& ff) {
 // One warp of CTA 0: the CTA partials of the previous step folded in index order
 // (lane l takes l, l + 32, ...; then the fixed butterfly) into the rank partial
 // and the barycentre output; zeroes the next step's key slot.
-__device__ __forceinline__ void fold_prev_outputs(const FastFold& ff, double* bary_out) {
+// (out of line: inlined into the step kernel it cost the hot loop 7 % more instructions -- register moves)
+__device__ __noinline__ void fold_prev_outputs(const Partial* bp_in, unsigned bp_in_count, Partial* fold_out,
+                                               unsigned long long* key_reset, double* bary_out) {
     const unsigned lane = threadIdx.x & 31;
     Partial f = identity();
-    for (unsigned i = lane; i < ff.bp_in_count; i += 32) fold(f, load_cg(&ff.bp_in[i]));
+    for (unsigned i = lane; i < bp_in_count; i += 32) fold(f, load_cg(&bp_in[i]));
     f = warp_reduce(f);
     if (lane == 0) {
-        store_partial(ff.fold_out, f);
+        store_partial(fold_out, f);
         if (bary_out) {
             bary_out[0] = f.sx;
             bary_out[1] = f.sy;
             bary_out[2] = f.sf;
         }
-        if (ff.key_reset) *ff.key_reset = 0ull;
+        if (key_reset) *key_reset = 0ull;
     }
 }
 
@@ -920,9 +922,6 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     __syncthreads();
 
     const unsigned lane = threadIdx.x & 31;
-    // the last warp of CTA 0 folds the previous step's CTA partials before it claims tiles (its
-    // share goes to the other warps)
-    if (split && blockIdx.x == 0 && threadIdx.x >= blockDim.x - 32) fold_prev_outputs(a.ff, a.bary_out);
     __shared__ Partial ragged_part;
     if (full) {
         dyn_tiles<kExplicitCur, kSane, true, true>(a, P, eat, M, step, rev, tile_part, next_tile, s_ghi, s_gpt,
@@ -964,6 +963,11 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     }
     __syncthreads();
     const unsigned long long t_done = (a.ec.out && threadIdx.x == 0) ? gtimer() : 0ull;
+    // Split fold, consumer side: the last warp of CTA 0 folds the PREVIOUS step's CTA partials into the
+    // outputs here, after the run (their buffer is rewritten by the next kernel at the earliest; folding
+    // before the tile loop cost the loop 7 % more instructions in register moves).
+    if (a.ff.key_in && blockIdx.x == 0 && threadIdx.x >= blockDim.x - 32)
+        fold_prev_outputs(a.ff.bp_in, a.ff.bp_in_count, a.ff.fold_out, a.ff.key_reset, a.bary_out);
     Partial cta = identity();
     if (threadIdx.x < 32) {
         for (unsigned i = lane; i < s_ntiles; i += 32) fold(cta, tile_part[i]);
@@ -1480,7 +1484,8 @@ __global__ void __launch_bounds__(kThreads) eat_kernel(const EatArgs a) {
     const bool split = a.ff.key_in != nullptr;
     const Partial prev = split ? prev_from_key(a.ff) : combine_prev(a.part_in, a.world, a.px);
     publish_prev(prev, a.trace_out, split ? nullptr : a.bary_out, a.ec, t_start);
-    if (split && blockIdx.x == 0 && threadIdx.x < 32) fold_prev_outputs(a.ff, a.bary_out);
+    if (split && blockIdx.x == 0 && threadIdx.x < 32)
+        fold_prev_outputs(a.ff.bp_in, a.ff.bp_in_count, a.ff.fold_out, a.ff.key_reset, a.bary_out);
     if (!(prev.best > 0.0)) return;  // sim.hpp:115: no improvement, weights unchanged
     const SharedDivisor M = make_divisor(prev.best);
     const double half = a.k.half_pond;

@@ -196,7 +196,7 @@ struct EatLink {
 // this kernel: two dependent L2 round trips and a block reduction off the
 // per-step chain).  The consumer (the next step kernel, or the trailing eat)
 // reads the key; one warp of its CTA 0 folds the CTA partials in index order
-// for the outputs (barycentre sums, the cached rank partial) beside the run.
+// for the outputs (barycentre sums, the cached rank partial) after its own run.
 // Key slots rotate over three steps (CTA 0 of step k zeroes step k+1's slot,
 // last read by step k-1's consumers), CTA-partial buffers over two.
 struct FastFold {
