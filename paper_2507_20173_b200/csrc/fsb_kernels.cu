@@ -889,37 +889,48 @@ __global__ void __launch_bounds__(kDynThreads, FSB_DYN_MIN_BLOCKS) step_kernel_d
     __shared__ unsigned next_tile, s_ghi, s_gpt, s_ntiles;
     const StepParams P = params_of(a.k);
     const unsigned long long t_start = (a.ec.phase && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
+    // Everything that does not depend on the previous kernel comes BEFORE the
+    // programmatic-dependency wait, in the shadow of that kernel's tail: the
+    // step index (written by the graph's first node, long complete), the tile
+    // geometry with its 64-bit divisions, the shared-memory bookkeeping.
+    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
+    const uint64_t n = a.n;
+    const uint64_t npairs = n >> 1;
+    const bool rev = a.alternate && (step & 1ull);
+    // balanced contiguous chunk of 32-pair groups (32-bit group indices: up
+    // to 2^37 fish per shard); tiles of gpt groups
+    // In-range launches of fewer than 2^32 pairs run the hot loop over FULL
+    // groups only; the ragged last group is warp 1 of CTA 0's (below).
+    auto lay_out = [&](bool full_groups) {
+        const uint64_t ngroups_all = full_groups ? npairs / 32 : (npairs + 31) / 32;
+        // stripes of gpt groups dealt round-robin to the CTAs (tile k of this CTA
+        // is stripe k * gridDim + blockIdx.x): every SM works on one moving front
+        unsigned gpt =
+            (unsigned)((ngroups_all + (uint64_t)gridDim.x * kDynTiles - 1) / ((uint64_t)gridDim.x * kDynTiles));
+        const unsigned min_groups = a.tile_groups ? a.tile_groups : kDynMinGroups;
+        if (gpt < min_groups) gpt = min_groups;  // claims + tile flushes amortised over >= min_groups groups
+        const unsigned nstripes = (unsigned)((ngroups_all + gpt - 1) / gpt);
+        if (threadIdx.x == 0) {
+            next_tile = 0;
+            s_ghi = (unsigned)ngroups_all;
+            s_gpt = gpt;
+            s_ntiles = nstripes > blockIdx.x ? (nstripes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+        }
+        __syncthreads();
+    };
+    // the expected mode: in-range state (kSane) with an in-range divisor, checked after the wait
+    const bool full_expected = FSB_DYN_FULL && FSB_DYN_FAST && kSane && (npairs >> 32) == 0;
+    lay_out(full_expected);
+
     pdl_wait_and_release();
     const bool split = a.ff.key_in != nullptr;  // split fold: the max from its key slot, the sums folded beside the run
     const Partial prev = split ? prev_from_key(a.ff) : combine_prev(a.part_in, a.world, a.px);
     publish_prev(prev, a.trace_out, split ? nullptr : a.bary_out, a.ec, t_start);
     const bool eat = prev.best > 0.0;  // sim.hpp:115
     const SharedDivisor M = make_divisor(eat ? prev.best : 1.0);
-    const uint64_t step = (a.step_ptr ? *a.step_ptr : 0ull) + a.step_add;
-    const uint64_t n = a.n;
-    const uint64_t npairs = n >> 1;
-    const bool rev = a.alternate && (step & 1ull);
-
-    // balanced contiguous chunk of 32-pair groups (32-bit group indices: up
-    // to 2^37 fish per shard); tiles of gpt groups
-    // In-range launches of fewer than 2^32 pairs run the hot loop over FULL
-    // groups only; the ragged last group is warp 1 of CTA 0's (below).
     const bool fast = FSB_DYN_FAST && no_guards<kSane>(eat, M);
     const bool full = FSB_DYN_FULL && fast && (npairs >> 32) == 0;
-    const uint64_t ngroups_all = full ? npairs / 32 : (npairs + 31) / 32;
-    // stripes of gpt groups dealt round-robin to the CTAs (tile k of this CTA
-    // is stripe k * gridDim + blockIdx.x): every SM works on one moving front
-    unsigned gpt = (unsigned)((ngroups_all + (uint64_t)gridDim.x * kDynTiles - 1) / ((uint64_t)gridDim.x * kDynTiles));
-    const unsigned min_groups = a.tile_groups ? a.tile_groups : kDynMinGroups;
-    if (gpt < min_groups) gpt = min_groups;  // claims + tile flushes amortised over >= min_groups groups
-    const unsigned nstripes = (unsigned)((ngroups_all + gpt - 1) / gpt);
-    if (threadIdx.x == 0) {
-        next_tile = 0;
-        s_ghi = (unsigned)ngroups_all;
-        s_gpt = gpt;
-        s_ntiles = nstripes > blockIdx.x ? (nstripes - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
-    }
-    __syncthreads();
+    if (full != full_expected) lay_out(full);  // an out-of-range divisor (another rank's state): the guarded loop's layout
 
     const unsigned lane = threadIdx.x & 31;
     __shared__ Partial ragged_part;
