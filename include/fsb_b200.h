@@ -78,8 +78,8 @@ typedef struct fsb_timing {
 
 /* Step-loop strategies. */
 enum fsb_strategy {
-    FSB_STRATEGY_AUTO = 0,       /* single GPU: persistent cluster up to 16384 fish, grid up to 2.5e6,
-                                    else stream; several ranks: stream */
+    FSB_STRATEGY_AUTO = 0,       /* single GPU: persistent cluster up to 16384 fish, grid while the school fits
+                                    in shared memory (~1.06e6 fish), else stream; several ranks: stream */
     FSB_STRATEGY_STREAM = 1,     /* one fused step kernel per step, CUDA-graph replayed  */
     FSB_STRATEGY_PERSISTENT = 2, /* one thread-block cluster runs all steps on chip       */
     FSB_STRATEGY_GRID = 3        /* one cooperative launch of the whole grid runs all steps (single GPU,
@@ -184,7 +184,8 @@ int fsb_engine_eat(fsb_engine* e, double* max_diff, double* seconds);
 /* The step loop of simulate (sim.hpp:139-144) for steps
  * [first_step, first_step + num_steps): T x (move, eat), on device.
  * Strategy AUTO: the persistent cluster kernel up to 16,384 fish, the
- * cooperative grid up to 2.5e6, else the graph of step kernels; if the device
+ * cooperative grid while the school fits in shared memory (about 1.06e6
+ * fish), else the graph of step kernels; if the device
  * refuses the co-resident launch the run falls back to the graph (see
  * fsb_engine_last_strategy).  An explicit PERSISTENT / GRID request fails
  * with FSB_ERR_UNSUPPORTED instead.

@@ -374,10 +374,13 @@ bool want_persistent(const fsb_engine* e) {
     return e->count > 0 && e->count <= 16384;
 }
 
-// FSB_STRATEGY_GRID, and AUTO for mid-size single-rank schools: the
-// cluster-reduced persistent grid kernel measured 3-13% faster than the graph
-// of step kernels from 2e4 to 2e6 fish and slower from 3e6
-// (profiles/r03_ab_grid.jsonl).
+// FSB_STRATEGY_GRID, and AUTO for single-rank schools that fit in shared memory
+// (fits_sgrid: about 1.06e6 fish).  Above that AUTO runs the graph of step
+// kernels: in round 1 the L2 cluster grid was 3-13 % faster than the graph up to
+// 2e6 fish (profiles/r03_ab_grid.jsonl); with the split fold and the pre-wait
+// prologue the graph is 0.5-7 % faster from 1.1e6 to 2.5e6
+// (profiles/round2_ab_graph_vs_l2_grid.jsonl).  With FSB_FLAG_L2_GRID or
+// FSB_FLAG_FLAT_GRID, AUTO still takes the grid up to this size.
 constexpr uint64_t kGridAutoMaxFish = 2500000;
 
 // The shared-memory-resident grid kernel holds the school on chip: every CTA's
@@ -400,7 +403,8 @@ bool tool_injected() {
 bool want_grid(const fsb_engine* e) {
     if (e->cur_explicit || e->world != 1 || e->use_nccl || e->peer_mode) return false;
     if (e->strategy == FSB_STRATEGY_GRID) return true;
-    return e->strategy == FSB_STRATEGY_AUTO && e->cgrid_nc > 0 && e->count > 16384 && e->count <= kGridAutoMaxFish &&
+    const bool asked_l2 = (e->flags & (FSB_FLAG_L2_GRID | FSB_FLAG_FLAT_GRID)) && e->count <= kGridAutoMaxFish;
+    return e->strategy == FSB_STRATEGY_AUTO && e->cgrid_nc > 0 && e->count > 16384 && (fits_sgrid(e) || asked_l2) &&
            !(e->flags & (FSB_FLAG_FORCE_BULK | FSB_FLAG_DYNAMIC_TILES | FSB_FLAG_STATIC_TILES));
 }
 

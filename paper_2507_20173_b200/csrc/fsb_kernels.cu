@@ -21,7 +21,7 @@
 //                   16,385 to ~1.06e6 fish: C0).
 //   cgrid_kernel    all T steps in one cooperative launch of 8-CTA clusters,
 //                   the school in L2, reducing over DSMEM before the grid-wide
-//                   exchange (AUTO ~1.06e6-2.5e6 fish; FSB_FLAG_L2_GRID).
+//                   exchange (FSB_FLAG_L2_GRID; AUTO's choice above the shared-memory grid until round 2).
 //   grid_kernel     the same without clusters (FSB_FLAG_FLAT_GRID).
 //   eat_kernel      the trailing / standalone weight update (sim.hpp:115-121).
 //   reduce_kernel   max + sums of the current state without moving it (eat()

@@ -798,11 +798,12 @@ def test_smem_grid_and_l2_grid_bit_exact(orc, n, t):
 
 
 # ---- AUTO at its thresholds ----------------------------------------------------------
-@pytest.mark.parametrize("n,want", [(16_384, "persistent"), (16_385, "grid"), (2_500_000, "grid"),
-                                    (2_500_001, "stream"), (2_999_999, "stream"), (3_000_000, "stream")])
+@pytest.mark.parametrize("n,want", [(16_384, "persistent"), (16_385, "grid"), (1_060_864, "grid"),
+                                    (1_060_866, "stream"), (2_500_000, "stream"), (3_000_000, "stream")])
 def test_auto_thresholds_bit_exact(orc, n, want):
-    """AUTO's choice at each boundary (persistent cluster <= 16,384 fish < grid
-    <= 2.5e6 < graph of claimed-tile step kernels):
+    """AUTO's choice at each boundary (persistent cluster <= 16,384 fish < the
+    shared-memory grid <= its capacity, 148 SMs x 3,584 pairs = 1,060,864 fish
+    < graph of claimed-tile step kernels):
     the strategy it runs and the oracle's state and trace on both sides."""
     cfg = fsb.baseline_config(n, 3)
     want_fish, want_trace = orc.simulate(ocfg(cfg))
