@@ -16,6 +16,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA sm_100 device (B200)")
     config.addinivalue_line("markers", "slow: long-running (large configs)")
+    config.addinivalue_line("markers", "timeout(seconds): per-test bound (pytest-timeout; a no-op without the plugin)")
 
 
 def unhex(h: str) -> float:

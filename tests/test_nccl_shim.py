@@ -26,7 +26,8 @@ import oracle
 import paper_2507_20173_b200 as fsb
 from conftest import ROOT, bits, unhex
 
-pytestmark = pytest.mark.gpu
+# multi-process tests: a bound, so a lost rank fails the test instead of stalling the suite
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
 
 SHIM = os.path.join(ROOT, "tests", "cpp", "libnccl_shim.so")
 BARY_RTOL = 1e-12

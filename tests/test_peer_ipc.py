@@ -21,7 +21,8 @@ import oracle
 import paper_2507_20173_b200 as fsb
 from conftest import ROOT
 
-pytestmark = pytest.mark.gpu
+# multi-process tests: a bound, so a lost rank fails the test instead of stalling the suite
+pytestmark = [pytest.mark.gpu, pytest.mark.timeout(900)]
 
 
 @pytest.fixture(scope="module", autouse=True)
