@@ -2,7 +2,7 @@
 random strategies, step kernels, split points and uploaded hand-built schools,
 and random shardings through the host exchange, each against the CPU oracle
 (bit-exact school and trace, barycentre within 1e-12).  The long runs are in
-profiles/round2_s6_fuzz_parity.jsonl (16,000 cases, 0 mismatches)."""
+profiles/round2_s6_fuzz_parity.jsonl and round2_s10_fuzz_parity_final_sources.jsonl (31,000 cases, 0 mismatches)."""
 import json
 import os
 import subprocess
